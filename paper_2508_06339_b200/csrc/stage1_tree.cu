@@ -1,0 +1,686 @@
+// stage1_tree.cu -- fast stage 1 (dense -> band) for sm_100a.
+//
+// Same tile operators as the reference stage 1 (bandreduce.py:31-120,
+// kernels.py:205-559): GEQRT on ts x ts tiles, a triangle-on-triangle TSQRT
+// (kernels.py:286-313 with B upper triangular), and WY-form UNMQR / TSMQR
+// trailing updates.  What changes is the panel's reduction tree: the
+// reference walks each panel as ONE flat TSQRT chain (critical path ~N^2
+// tile QRs per matrix); here every panel tile is factored
+// in parallel and the R factors are combined by a binary tree (depth
+// ceil(log2 m)).  The orthogonal factor differs from the reference's, the
+// band differs, the singular values do not (parity is on values).
+//
+// Per sweep side (RQ on the matrix, LQ on its lazy transpose -- a stride
+// swap, no copy) there are exactly two launches:
+//
+//  k_panel_tree   one CTA per panel tile.  Leaf: Householder QR of the tile
+//                 in shared memory (reference reflector scalars, incl. the
+//                 10*eps guard), then the compact-WY factor T (larft) and
+//                 U = V T^T.  Tree: the second child CTA to arrive at a node
+//                 (atomic arrival counter) combines [R_left; R_right] with a
+//                 TT-QR and climbs; the root writes R into the band tile.
+//  k_trail_tree   one CTA per CB-column block of the trailing matrix.  Walks
+//                 the same tree in post-order with an on-chip stack of
+//                 ts x CB tiles, so every trailing tile is read once and
+//                 written once per sweep side:
+//                   leaf:  W = V^T X;                 X -= U W
+//                   node:  W = X_top + V^T X_bot;     X_top -= T^T W;
+//                          X_bot -= U W
+//                 Each product is a register-blocked FMA GEMM (K = ts) with
+//                 the ts x ts operand streamed through shared memory.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace bsvd {
+
+constexpr int kNT = 256;          // threads per CTA for both kernels
+
+template <typename C> struct TileCfg {
+    // trailing column-block width: a ts x CB tile is 16 KiB
+    static constexpr int elems = 16384 / (int)sizeof(C);
+};
+
+__host__ __device__ inline int64_t tree_count(int64_t m, int j) {  // nodes at level j
+    return (m + ((int64_t)1 << j) - 1) >> j;
+}
+__host__ __device__ inline int tree_levels(int64_t m) {           // ceil(log2 m)
+    int L = 0;
+    while (((int64_t)1 << L) < m) ++L;
+    return L;
+}
+__host__ __device__ inline int64_t tree_offset(int64_t m, int j) { // first slot of level j
+    int64_t off = 0;
+    for (int q = 0; q < j; ++q) off += tree_count(m, q);
+    return off;
+}
+
+// Workspace of one sweep side for one matrix:
+//   node slots (<= 2N): Vk | Um | Tt   (3 ts^2 C each)
+//   R slots (N): ts^2 C each
+//   arrival counters (N ints)
+template <typename C>
+struct TreeWs {
+    C *nodes;   // slot s at nodes + s * 3 * ts2
+    C *R;       // leaf l at R + l * ts2
+    int *cnt;
+    int64_t ts2;
+    __host__ __device__ C *Vk(int64_t s) const { return nodes + s * 3 * ts2; }
+    __host__ __device__ C *Um(int64_t s) const { return nodes + s * 3 * ts2 + ts2; }
+    __host__ __device__ C *Tt(int64_t s) const { return nodes + s * 3 * ts2 + 2 * ts2; }
+};
+
+template <typename C>
+__host__ __device__ inline size_t tree_ws_elems(int64_t N, int ts) {
+    const int64_t ts2 = (int64_t)ts * ts;
+    return (size_t)(2 * N * 3 * ts2 + N * ts2) + (size_t)(N + 64) * sizeof(int) / sizeof(C) + 64;
+}
+
+template <typename C>
+__device__ __forceinline__ C warp_sum_t(C v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename C, int G>
+__device__ __forceinline__ C group_sum(C v) {   // sum over G consecutive lanes
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Leaf: Householder QR of one ts x ts tile held column-major in smem (ld =
+// ts+1), reference reflector scalars.  Afterwards: R in the upper triangle,
+// v (unit implied) strictly below, tau[] in smem.
+template <typename C, int TS>
+__device__ void leaf_qr(C *A, C *tau, C *scal) {
+    constexpr int LD = TS + 1;
+    constexpr int TPC = (kNT / TS) < 32 ? (kNT / TS) : 32;   // threads per column
+    const C two = C(2), eps10 = C(10) * Eps<C>::v;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int kk = 0; kk < TS - 1; ++kk) {
+        if (warp == 0) {
+            C sig = C(0);
+            for (int r = kk + 1 + lane; r < TS; r += 32) sig += A[kk * LD + r] * A[kk * LD + r];
+            sig = warp_sum_t(sig);
+            const C alpha = A[kk * LD + kk];
+            C x, t, rhop;
+            reflector_scalars(alpha, sig, alpha, sig, eps10, two, x, t, rhop);
+            for (int r = kk + 1 + lane; r < TS; r += 32) A[kk * LD + r] = A[kk * LD + r] / x;
+            if (lane == 0) {
+                A[kk * LD + kk] = alpha - rhop;
+                tau[kk] = t;
+            }
+        }
+        __syncthreads();
+        const C t = tau[kk];
+        // columns c > kk: TPC threads per column
+        const int g = tid / TPC, q = tid % TPC;
+        for (int cb = kk + 1; cb < TS; cb += kNT / TPC) {   // warp-uniform trip count
+            const int c = cb + g;
+            const bool act = c < TS;
+            C w = C(0);
+            if (act)
+                for (int r = kk + 1 + q; r < TS; r += TPC) w += A[kk * LD + r] * A[c * LD + r];
+            w = group_sum<C, TPC>(w);
+            if (act) {
+                w = (w + A[c * LD + kk]) * t;
+                for (int r = kk + 1 + q; r < TS; r += TPC) A[c * LD + r] -= w * A[kk * LD + r];
+                if (q == 0) A[c * LD + kk] -= w;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) tau[TS - 1] = C(0);   // A8: last tile column has no reflector
+    __syncthreads();
+    (void)scal;
+}
+
+// T (upper, compact WY, forward columnwise) from G = V^T V and tau.
+// getG(i, j) for i < j, Tset/Tget store T(i, j) for i <= j.  tmp: ts vector.
+template <typename C, int TS, typename GetG, typename TGet, typename TSet>
+__device__ void build_T(const C *tau, C *tmp, GetG getG, TGet tget, TSet tset) {
+    const int tid = threadIdx.x;
+    for (int j = 0; j < TS; ++j) {
+        for (int i = tid; i < j; i += kNT) tmp[i] = getG(i, j);
+        __syncthreads();
+        C v = C(0);
+        if (tid < j) {
+            C s = C(0);
+            for (int q = tid; q < j; ++q) s += tget(tid, q) * tmp[q];
+            v = -tau[j] * s;
+        }
+        __syncthreads();
+        if (tid < j) tset(tid, j, v);
+        if (tid == 0) tset(j, j, tau[j]);
+        __syncthreads();
+    }
+}
+
+// Packed upper-triangular column-major index (r <= c).
+__host__ __device__ __forceinline__ int pk(int r, int c) { return c * (c + 1) / 2 + r; }
+
+// TT-QR of [R_top; R_bot], both upper triangular, packed in smem.  After:
+// R_top updated, R_bot holds V_b (upper), tau[].  Reference TSQRT scalars.
+template <typename C, int TS>
+__device__ void tt_qr(C *Rt, C *Rb, C *tau, C *scal) {
+    const C two = C(2), eps10 = C(10) * Eps<C>::v;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int kk = 0; kk < TS; ++kk) {
+        if (warp == 0) {
+            C sig = C(0);
+            for (int r = lane; r <= kk; r += 32) sig += Rb[pk(r, kk)] * Rb[pk(r, kk)];
+            sig = warp_sum_t(sig);
+            const C alpha = Rt[pk(kk, kk)];
+            C x, t, rhop;
+            reflector_scalars(alpha, sig, alpha, sig, eps10, two, x, t, rhop);
+            for (int r = lane; r <= kk; r += 32) Rb[pk(r, kk)] = Rb[pk(r, kk)] / x;
+            if (lane == 0) {
+                Rt[pk(kk, kk)] = alpha - rhop;
+                tau[kk] = t;
+            }
+        }
+        __syncthreads();
+        const C t = tau[kk];
+        constexpr int TPC = (kNT / TS) < 32 ? (kNT / TS) : 32;
+        const int g = tid / TPC, q = tid % TPC;
+        for (int cb = kk + 1; cb < TS; cb += kNT / TPC) {   // warp-uniform trip count
+            const int c = cb + g;
+            const bool act = c < TS;
+            C w = C(0);
+            if (act)
+                for (int r = q; r <= kk; r += TPC) w += Rb[pk(r, kk)] * Rb[pk(r, c)];
+            w = group_sum<C, TPC>(w);
+            if (act) {
+                w = (w + Rt[pk(kk, c)]) * t;
+                for (int r = q; r <= kk; r += TPC) Rb[pk(r, c)] -= w * Rb[pk(r, kk)];
+                if (q == 0) Rt[pk(kk, c)] -= w;
+            }
+        }
+        __syncthreads();
+    }
+    (void)scal;
+}
+
+// View helpers: tile (tr, tc) of the (possibly transposed) matrix view.
+template <typename S>
+struct View {
+    S *base;
+    int64_t rs, cs;
+    __device__ __forceinline__ S *ptr(int64_t r, int64_t c) const { return base + r * rs + c * cs; }
+};
+
+// ---------------------------------------------------------------------------
+// Panel kernel.  Grid: m CTAs (tile rows top..top+m-1 of view tile column k).
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_t top, int64_t k,
+                                                   TreeWs<C> ws, int64_t ws_bstride,
+                                                   int64_t a_bstride) {
+    using CV = Conv<S, C>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *sm = (C *)smem_raw;
+    constexpr int LD = TS + 1;
+    constexpr int PK = TS * (TS + 1) / 2;
+    // layout: [ big: max(TS*LD, 3*PK) ] [tau TS] [tmp TS] [scal 8]
+    constexpr int BIG = (TS * LD > 3 * PK) ? TS * LD : 3 * PK;
+    C *tau = sm + BIG;
+    C *tmp = tau + TS;
+    C *scal = tmp + TS;
+    __shared__ int s_old;
+
+    const int64_t b = blockIdx.y;
+    V.base += b * a_bstride;
+    ws.nodes += b * ws_bstride;
+    ws.R += b * ws_bstride;
+    ws.cnt = (int *)((char *)ws.cnt + b * ws_bstride * (int64_t)sizeof(C));
+    const int64_t l = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS;
+
+    // ---- leaf: GEQRT of view tile (top + l, k) ----
+    {
+        C *A = sm;
+        const int64_t r0 = (top + l) * TS, c0 = k * TS;
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            int r, c;
+            if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
+            A[c * LD + r] = CV::ld(*V.ptr(r0 + r, c0 + c));
+        }
+        __syncthreads();
+        leaf_qr<C, TS>(A, tau, scal);
+        // R -> ws.R[l] (column-major, upper triangle + zeros)
+        C *Rg = ws.R + l * ts2;
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            const int c = idx / TS, r = idx % TS;
+            Rg[idx] = (r <= c) ? A[c * LD + r] : C(0);
+        }
+        __syncthreads();
+        // G (i<j) into the upper triangle (R saved), then T in place, tau on the diagonal.
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            const int j = idx / TS, i = idx % TS;
+            if (i < j) {
+                C s = A[i * LD + j];   // V[j][i]
+                for (int r = j + 1; r < TS; ++r) s += A[i * LD + r] * A[j * LD + r];
+                A[j * LD + i] = s;
+            }
+        }
+        __syncthreads();
+        build_T<C, TS>(tau, tmp,
+                       [&](int i, int j) { return A[j * LD + i]; },
+                       [&](int i, int j) { return A[j * LD + i]; },
+                       [&](int i, int j, C v) { A[j * LD + i] = v; });
+        // Vk[r][i] = V(r, i);  Um[i][r] = U(r, i) = sum_{j=i..r} V(r,j) T(i,j)
+        C *Vk = ws.Vk(l), *Um = ws.Um(l);
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            const int r = idx / TS, i = idx % TS;
+            Vk[idx] = (r > i) ? A[i * LD + r] : (r == i ? C(1) : C(0));
+        }
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            const int i = idx / TS, r = idx % TS;
+            C s = C(0);
+            if (r >= i) {
+                s = A[i * LD + i] * ((r == i) ? C(1) : A[i * LD + r]);   // j = i: T(i,i)=tau_i
+                for (int j = i + 1; j <= r; ++j) s += ((j == r) ? C(1) : A[j * LD + r]) * A[j * LD + i];
+            }
+            Um[idx] = s;
+        }
+    }
+
+    // ---- tree: climb while we are the second arrival ----
+    const int L = tree_levels(m);
+    int64_t node = l;   // index at current level
+    for (int j = 1; j <= L; ++j) {
+        const int64_t parent = node >> 1;
+        const bool has_right = ((parent << 1) + 1) < tree_count(m, j - 1);
+        if (has_right) {
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                int *c = ws.cnt + tree_offset(m, j) - m + parent;   // level>=1 counters
+                s_old = atomicAdd(c, 1);
+                if (s_old == 1) *c = 0;   // self-cleaning for the next launch
+                __threadfence();
+            }
+            __syncthreads();
+            if (s_old == 0) return;   // first arrival: the sibling continues
+            // combine: left leaf slot a = (2*parent) << (j-1), right b = (2*parent+1) << (j-1)
+            const int64_t a = (parent << 1) << (j - 1);
+            const int64_t bb = ((parent << 1) + 1) << (j - 1);
+            C *Rt = sm, *Rb = sm + PK, *Tp = sm + 2 * PK;
+            const C *Ra_g = ws.R + a * ts2, *Rb_g = ws.R + bb * ts2;
+            for (int idx = tid; idx < TS * TS; idx += kNT) {
+                const int c = idx / TS, r = idx % TS;
+                if (r <= c) {
+                    Rt[pk(r, c)] = __ldcg(Ra_g + idx);
+                    Rb[pk(r, c)] = __ldcg(Rb_g + idx);
+                }
+            }
+            __syncthreads();
+            tt_qr<C, TS>(Rt, Rb, tau, scal);
+            // R_top -> slot a
+            C *Rg = ws.R + a * ts2;
+            for (int idx = tid; idx < TS * TS; idx += kNT) {
+                const int c = idx / TS, r = idx % TS;
+                Rg[idx] = (r <= c) ? Rt[pk(r, c)] : C(0);
+            }
+            // G(i,j) = sum_{r<=i} Vb(r,i) Vb(r,j) into Tp, then T in place
+            for (int idx = tid; idx < TS * TS; idx += kNT) {
+                const int jj = idx / TS, i = idx % TS;
+                if (i < jj) {
+                    C s = C(0);
+                    for (int r = 0; r <= i; ++r) s += Rb[pk(r, i)] * Rb[pk(r, jj)];
+                    Tp[pk(i, jj)] = s;
+                }
+            }
+            __syncthreads();
+            build_T<C, TS>(tau, tmp,
+                           [&](int i, int jj) { return Tp[pk(i, jj)]; },
+                           [&](int i, int jj) { return Tp[pk(i, jj)]; },
+                           [&](int i, int jj, C v) { Tp[pk(i, jj)] = v; });
+            const int64_t slot = tree_offset(m, j) + parent;
+            C *Vk = ws.Vk(slot), *Um = ws.Um(slot), *Tt = ws.Tt(slot);
+            for (int idx = tid; idx < TS * TS; idx += kNT) {
+                const int r = idx / TS, i = idx % TS;   // Vk[r][i] = Vb(r,i); Tt[r][i] = T(r,i)
+                Vk[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
+                Tt[idx] = (r <= i) ? Tp[pk(r, i)] : C(0);
+            }
+            for (int idx = tid; idx < TS * TS; idx += kNT) {
+                const int i = idx / TS, r = idx % TS;   // Um[i][r] = U(r,i) = sum_{jj>=max(i,r)} Vb(r,jj) T(i,jj)
+                C s = C(0);
+                for (int jj = (i > r ? i : r); jj < TS; ++jj) s += Rb[pk(r, jj)] * Tp[pk(i, jj)];
+                Um[idx] = s;
+            }
+        }
+        node = parent;
+    }
+    // root: R of the whole panel (slot 0) -> upper triangle of view tile (top, k)
+    __syncthreads();
+    if (L == 0 || node == 0) {
+        const C *Rg = ws.R;   // leaf slot 0
+        const int64_t r0 = top * TS, c0 = k * TS;
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            int r, c;
+            if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
+            if (r <= c) *V.ptr(r0 + r, c0 + c) = CV::st(__ldcg(Rg + c * TS + r));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Trailing kernel helpers.
+//   acc[MR][NR] (+)= sum_k Ag[k][m] * Bs[k][c]   over the thread's microtile
+// Ag: global ts x ts operand in [k][m] layout (m fastest), streamed through
+// two smem chunk buffers of KC x TS.  Bs: smem [TS][CBP].
+template <typename C, int TS, int CB, int MR, int NR, int KC>
+__device__ __forceinline__ void gemm_acc(const C *__restrict__ Ag, const C *Bs, C *Abuf,
+                                         C (&acc)[MR][NR], int tm, int tc) {
+    constexpr int CBP = CB;
+    constexpr int NCH = TS / KC;
+    constexpr int CHUNK = KC * TS;
+    constexpr int PER = (CHUNK + kNT - 1) / kNT;
+    const int tid = threadIdx.x;
+    C pre[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * kNT;
+        pre[q] = (idx < CHUNK) ? __ldcg(Ag + idx) : C(0);
+    }
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+        C *buf = Abuf + (ch & 1) * CHUNK;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = tid + q * kNT;
+            if (idx < CHUNK) buf[idx] = pre[q];
+        }
+        __syncthreads();
+        if (ch + 1 < NCH) {
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int idx = tid + q * kNT;
+                pre[q] = (idx < CHUNK) ? __ldcg(Ag + (ch + 1) * CHUNK + idx) : C(0);
+            }
+        }
+#pragma unroll 4
+        for (int kk = 0; kk < KC; ++kk) {
+            C a[MR], bv[NR];
+#pragma unroll
+            for (int i = 0; i < MR; ++i) a[i] = buf[kk * TS + tm * MR + i];
+#pragma unroll
+            for (int jx = 0; jx < NR; ++jx) bv[jx] = Bs[(ch * KC + kk) * CBP + tc * NR + jx];
+#pragma unroll
+            for (int i = 0; i < MR; ++i)
+#pragma unroll
+                for (int jx = 0; jx < NR; ++jx) acc[i][jx] += a[i] * bv[jx];
+        }
+        // the next iteration writes the other buffer; this one is rewritten
+        // two chunks later, after the __syncthreads above.
+    }
+    __syncthreads();
+}
+
+template <typename S, typename C, int TS, int CB>
+__device__ __forceinline__ void load_tile(const View<S> &V, int64_t r0, int64_t c0, int64_t cmax,
+                                          C *X) {
+    using CV = Conv<S, C>;
+    for (int idx = threadIdx.x; idx < TS * CB; idx += kNT) {
+        int r, c;
+        if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % CB; r = idx / CB; }
+        X[r * CB + c] = (c0 + c < cmax) ? CV::ld(*V.ptr(r0 + r, c0 + c)) : C(0);
+    }
+}
+
+template <typename S, typename C, int TS, int CB>
+__device__ __forceinline__ void store_tile(const View<S> &V, int64_t r0, int64_t c0, int64_t cmax,
+                                           const C *X) {
+    using CV = Conv<S, C>;
+    for (int idx = threadIdx.x; idx < TS * CB; idx += kNT) {
+        int r, c;
+        if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % CB; r = idx / CB; }
+        if (c0 + c < cmax) *V.ptr(r0 + r, c0 + c) = CV::st(X[r * CB + c]);
+    }
+}
+
+// Trailing kernel.  Grid: ceil(ncols / CB) column blocks of the view's
+// trailing columns [k+1)*TS, N*TS); rows top..top+m-1 (tile rows).
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(kNT) k_trail_tree(View<S> V, int64_t m, int64_t top, int64_t k,
+                                                   int64_t ncols, TreeWs<C> ws,
+                                                   int64_t ws_bstride, int64_t a_bstride) {
+    constexpr int CB = TileCfg<C>::elems / TS;
+    constexpr int MR = 4;
+    constexpr int NR = (TS * CB) / (kNT * MR);   // 4 (fp32) / 2 (fp64)
+    constexpr int KC = (TS >= 16) ? 16 : TS;
+    constexpr int TILE = TS * CB;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *sm = (C *)smem_raw;
+    C *Abuf = sm;                   // 2 * KC * TS
+    C *W = Abuf + 2 * KC * TS;      // TILE
+    C *stack = W + TILE;            // depth * TILE
+    __shared__ int st_lvl[24];
+    __shared__ int64_t st_idx[24];
+
+    const int64_t b = blockIdx.y;
+    V.base += b * a_bstride;
+    ws.nodes += b * ws_bstride;
+    const int tid = threadIdx.x;
+    const int tm = tid % (TS / MR), tc = tid / (TS / MR);
+    const int64_t c0 = (int64_t)blockIdx.x * CB;          // relative to first trailing column
+    const int64_t cbase = (k + 1) * TS;
+    const int64_t cmax = cbase + ncols;
+    const int L = tree_levels(m);
+    int sp = 0;
+
+    for (int64_t l = 0; l < m; ++l) {
+        C *X = stack + sp * TILE;
+        load_tile<S, C, TS, CB>(V, (top + l) * TS, cbase + c0, cmax, X);
+        __syncthreads();
+        // leaf: W = V^T X ; X -= U W
+        {
+            C acc[MR][NR];
+#pragma unroll
+            for (int i = 0; i < MR; ++i)
+#pragma unroll
+                for (int jx = 0; jx < NR; ++jx) acc[i][jx] = C(0);
+            gemm_acc<C, TS, CB, MR, NR, KC>(ws.Vk(l), X, Abuf, acc, tm, tc);
+#pragma unroll
+            for (int i = 0; i < MR; ++i)
+#pragma unroll
+                for (int jx = 0; jx < NR; ++jx) W[(tm * MR + i) * CB + tc * NR + jx] = acc[i][jx];
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < MR; ++i)
+#pragma unroll
+                for (int jx = 0; jx < NR; ++jx) acc[i][jx] = C(0);
+            gemm_acc<C, TS, CB, MR, NR, KC>(ws.Um(l), W, Abuf, acc, tm, tc);
+#pragma unroll
+            for (int i = 0; i < MR; ++i)
+#pragma unroll
+                for (int jx = 0; jx < NR; ++jx) X[(tm * MR + i) * CB + tc * NR + jx] -= acc[i][jx];
+            __syncthreads();
+        }
+        if (tid == 0) { st_lvl[sp] = 0; st_idx[sp] = l; }
+        __syncthreads();
+        ++sp;
+        // reduce the stack
+        while (true) {
+            const int j = st_lvl[sp - 1];
+            const int64_t i = st_idx[sp - 1];
+            if (j >= L) break;                      // root reached
+            if (i & 1) {                            // right child: combine with the entry below
+                C *Xt = stack + (sp - 2) * TILE, *Xb = stack + (sp - 1) * TILE;
+                const int64_t slot = tree_offset(m, j + 1) + (i >> 1);
+                C acc[MR][NR];
+                // W = X_top + Vb^T X_bot
+#pragma unroll
+                for (int ii = 0; ii < MR; ++ii)
+#pragma unroll
+                    for (int jx = 0; jx < NR; ++jx) acc[ii][jx] = Xt[(tm * MR + ii) * CB + tc * NR + jx];
+                gemm_acc<C, TS, CB, MR, NR, KC>(ws.Vk(slot), Xb, Abuf, acc, tm, tc);
+#pragma unroll
+                for (int ii = 0; ii < MR; ++ii)
+#pragma unroll
+                    for (int jx = 0; jx < NR; ++jx) W[(tm * MR + ii) * CB + tc * NR + jx] = acc[ii][jx];
+                __syncthreads();
+                // X_top -= T^T W
+#pragma unroll
+                for (int ii = 0; ii < MR; ++ii)
+#pragma unroll
+                    for (int jx = 0; jx < NR; ++jx) acc[ii][jx] = C(0);
+                gemm_acc<C, TS, CB, MR, NR, KC>(ws.Tt(slot), W, Abuf, acc, tm, tc);
+#pragma unroll
+                for (int ii = 0; ii < MR; ++ii)
+#pragma unroll
+                    for (int jx = 0; jx < NR; ++jx) Xt[(tm * MR + ii) * CB + tc * NR + jx] -= acc[ii][jx];
+                // X_bot -= U W
+#pragma unroll
+                for (int ii = 0; ii < MR; ++ii)
+#pragma unroll
+                    for (int jx = 0; jx < NR; ++jx) acc[ii][jx] = C(0);
+                gemm_acc<C, TS, CB, MR, NR, KC>(ws.Um(slot), W, Abuf, acc, tm, tc);
+#pragma unroll
+                for (int ii = 0; ii < MR; ++ii)
+#pragma unroll
+                    for (int jx = 0; jx < NR; ++jx) Xb[(tm * MR + ii) * CB + tc * NR + jx] -= acc[ii][jx];
+                __syncthreads();
+                // X_bot is final: its leaf is the leftmost leaf of node (j, i)
+                store_tile<S, C, TS, CB>(V, (top + (i << j)) * TS, cbase + c0, cmax, Xb);
+                __syncthreads();
+                --sp;
+                if (tid == 0) { st_lvl[sp - 1] = j + 1; st_idx[sp - 1] = i >> 1; }
+                __syncthreads();
+            } else if (i + 1 < tree_count(m, j)) {
+                break;                              // wait for the right sibling
+            } else {
+                if (tid == 0) { st_lvl[sp - 1] = j + 1; st_idx[sp - 1] = i >> 1; }   // pass-through
+                __syncthreads();
+            }
+        }
+    }
+    // root tile = leaf 0 (top tile row)
+    store_tile<S, C, TS, CB>(V, top * TS, cbase + c0, cmax, stack);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+template <typename C, int TS>
+constexpr size_t panel_smem() {
+    constexpr int LD = TS + 1;
+    constexpr int PK = TS * (TS + 1) / 2;
+    constexpr int BIG = (TS * LD > 3 * PK) ? TS * LD : 3 * PK;
+    return (size_t)(BIG + 2 * TS + 8) * sizeof(C);
+}
+template <typename C, int TS>
+size_t trail_smem(int depth) {
+    constexpr int CB = TileCfg<C>::elems / TS;
+    constexpr int KC = (TS >= 16) ? 16 : TS;
+    return (size_t)(2 * KC * TS + (size_t)(depth + 1) * TS * CB) * sizeof(C);
+}
+
+template <typename S, typename C>
+size_t tree_workspace_bytes(int64_t n, int ts) {
+    const int64_t N = n / ts;
+    return tree_ws_elems<C>(N, ts) * sizeof(C) + 256;
+}
+
+template <typename S, typename C, int TS>
+static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, void *wsp,
+                            cudaStream_t st, cudaEvent_t *ev_p, cudaEvent_t *ev_t, double *pms,
+                            double *tms) {
+    const int64_t N = n / TS;
+    const int64_t ws_elems = (int64_t)tree_ws_elems<C>(N, TS);
+    const int64_t ts2 = (int64_t)TS * TS;
+    TreeWs<C> ws;
+    ws.nodes = (C *)wsp;
+    ws.R = ws.nodes + 2 * N * 3 * ts2;
+    ws.cnt = (int *)(ws.R + N * ts2);
+    ws.ts2 = ts2;
+    cudaError_t err;
+    for (int64_t b = 0; b < batch; ++b) {
+        err = cudaMemsetAsync((char *)ws.cnt + b * ws_elems * (int64_t)sizeof(C), 0,
+                              (size_t)(N + 64) * sizeof(int), st);
+        if (err != cudaSuccess) return err;
+    }
+    const int depth = tree_levels(N) + 1;
+    const size_t psm = panel_smem<C, TS>();
+    const size_t tsm = trail_smem<C, TS>(depth);
+    if (tsm > 220 * 1024 || psm > 220 * 1024) return cudaErrorInvalidConfiguration;
+    static size_t psm_set = 0, tsm_set = 0;   // per instantiation
+    if (psm > psm_set) {
+        err = cudaFuncSetAttribute(k_panel_tree<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+        if (err != cudaSuccess) return err;
+        psm_set = psm;
+    }
+    if (tsm > tsm_set) {
+        err = cudaFuncSetAttribute(k_trail_tree<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        if (err != cudaSuccess) return err;
+        tsm_set = tsm;
+    }
+    constexpr int CB = TileCfg<C>::elems / TS;
+    auto side = [&](int64_t k, bool lq) -> cudaError_t {
+        View<S> V{a, lq ? n : 1, lq ? 1 : n};
+        const int64_t top = lq ? k + 1 : k;
+        if (top >= N) return cudaSuccess;
+        const int64_t m = N - top;
+        const int64_t ntrail = N - 1 - k;
+        if (ev_p) cudaEventRecord(ev_p[0], st);
+        k_panel_tree<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
+            V, m, top, k, ws, ws_elems, a_bstride);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if (ev_p) {
+            cudaEventRecord(ev_p[1], st);
+        }
+        if (ntrail > 0) {
+            const int64_t ncols = ntrail * TS;
+            k_trail_tree<S, C, TS><<<dim3((unsigned)((ncols + CB - 1) / CB), (unsigned)batch), kNT, tsm, st>>>(
+                V, m, top, k, ncols, ws, ws_elems, a_bstride);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+        if (ev_p) {
+            cudaEventRecord(ev_t[1], st);
+            cudaEventSynchronize(ev_t[1]);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev_p[0], ev_p[1]);
+            *pms += ms;
+            cudaEventElapsedTime(&ms, ev_p[1], ev_t[1]);
+            *tms += ms;
+        }
+        return cudaSuccess;
+    };
+    for (int64_t k = 0; k < N - 1; ++k) {
+        if ((err = side(k, false)) != cudaSuccess) return err;
+        if ((err = side(k, true)) != cudaSuccess) return err;
+    }
+    return side(N - 1, false);
+}
+
+template <typename S, typename C>
+cudaError_t banddiag_tree(S *a, int64_t n, int ts, int64_t batch, int64_t a_bstride, void *ws,
+                          cudaStream_t st, cudaEvent_t *ev_panel, cudaEvent_t *ev_trail,
+                          double *panel_ms, double *trail_ms) {
+    switch (ts) {
+    case 4: return run_tree<S, C, 4>(a, n, batch, a_bstride, ws, st, ev_panel, ev_trail, panel_ms, trail_ms);
+    case 8: return run_tree<S, C, 8>(a, n, batch, a_bstride, ws, st, ev_panel, ev_trail, panel_ms, trail_ms);
+    case 16: return run_tree<S, C, 16>(a, n, batch, a_bstride, ws, st, ev_panel, ev_trail, panel_ms, trail_ms);
+    case 32: return run_tree<S, C, 32>(a, n, batch, a_bstride, ws, st, ev_panel, ev_trail, panel_ms, trail_ms);
+    case 64: return run_tree<S, C, 64>(a, n, batch, a_bstride, ws, st, ev_panel, ev_trail, panel_ms, trail_ms);
+    case 128: return run_tree<S, C, 128>(a, n, batch, a_bstride, ws, st, ev_panel, ev_trail, panel_ms, trail_ms);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+#define INST(S, C)                                                                               \
+    template size_t tree_workspace_bytes<S, C>(int64_t, int);                                     \
+    template cudaError_t banddiag_tree<S, C>(S *, int64_t, int, int64_t, int64_t, void *,          \
+                                             cudaStream_t, cudaEvent_t *, cudaEvent_t *, double *, \
+                                             double *);
+INST(double, double)
+INST(float, float)
+INST(__half, float)
+#undef INST
+
+}  // namespace bsvd

@@ -1,0 +1,198 @@
+"""GPU parity: the sm_100a engine (through libbsvd.so's C ABI) against the
+reference's golden vectors and the C oracle.
+
+* faithful tile kernels and the faithful stage-1 driver: BIT-identical to the
+  reference (same bytes as tests/golden, produced by the reference itself);
+* stage 3 (bisection) and stage 2 (Householder chase): values within the
+  k*n*eps*||A||_2 bound of tests/tolerances.py;
+* full pipeline (fast tree stage 1 and faithful stage 1): values within the
+  bound against the reference values, every precision and edge case.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden, same_bits
+from tolerances import assert_close, bound, errors
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2508_06339_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def be_tree(P):
+    return P.B200Backend(stage1="tree")
+
+
+@pytest.fixture(scope="module")
+def be_faithful(P):
+    return P.B200Backend(stage1="faithful")
+
+
+class _K:
+    def __init__(self, name):
+        self.__name__ = name
+
+
+# ---- kernel level: bit-faithful reference tile kernels --------------------
+
+@pytest.mark.parametrize("name", golden_names("geqrt_"))
+def test_geqrt_kernel_bitwise(P, be_tree, name):
+    g = load_golden(name)
+    tile = np.asfortranarray(g["a"].copy())
+    tau = np.zeros(tile.shape[0], g["tau"].dtype)
+    be_tree.launch(_K("geqrt_kernel"), None, (tile, tau, None, None, None))
+    assert same_bits(tile, np.asfortranarray(g["out"]))
+    assert same_bits(tau, g["tau"])
+
+
+def test_tsqrt_identity_stack(P, be_tree):
+    g = load_golden("tsqrt_identity_stack")
+    r = np.asfortranarray(np.eye(4))
+    b = np.asfortranarray(np.eye(4))
+    tau = np.zeros(4)
+    be_tree.launch(_K("tsqrt_kernel"), None, (r, [b], [tau], None, None, None))
+    assert same_bits(r, np.asfortranarray(g["r"]))
+    assert same_bits(b, np.asfortranarray(g["b"]))
+    assert same_bits(tau, g["tau"])
+
+
+# ---- stage 1 faithful: band bit-identical to the reference ----------------
+
+@pytest.mark.parametrize("name", golden_names("pipe_"))
+def test_faithful_band_bitwise(P, be_faithful, name):
+    g = load_golden(name)
+    ts = int(g["ts"])
+    band = P.banddiag(g["a"], P.KernelConfig(tilesize=ts), backend=be_faithful)
+    assert same_bits(np.asfortranarray(band), np.asfortranarray(g["band"]))
+
+
+# ---- stage 3: bisection ----------------------------------------------------
+
+@pytest.mark.parametrize("name", golden_names("bidiag_"))
+def test_bidiagonal_values(P, be_tree, name):
+    g = load_golden(name)
+    got = P.bidiagonal_values(g["d"], g["e"], backend=be_tree)
+    assert got.dtype == np.float64
+    assert np.all(np.diff(got) <= 0)
+    assert_close(got, g["vals"], np.float64, g["d"].size, what=name)
+
+
+def test_bidiagonal_known_answers_exact(P, be_tree):
+    assert np.array_equal(P.bidiagonal_values([3.0, 2.0, 1.0], [0.0, 0.0], backend=be_tree), [3.0, 2.0, 1.0])
+    assert np.array_equal(P.bidiagonal_values([1.0, 0.0], [0.0], backend=be_tree), [1.0, 0.0])
+    got = P.bidiagonal_values([1.0, 1.0], [1.0], backend=be_tree)
+    assert np.allclose(got, [(1 + 5 ** 0.5) / 2, (5 ** 0.5 - 1) / 2], rtol=1e-14, atol=0)
+
+
+def test_bidiagonal_scaling_bitwise(P, be_tree):
+    rng = np.random.default_rng(3)
+    d, e = rng.standard_normal(77), rng.standard_normal(76)
+    v = P.bidiagonal_values(d, e, backend=be_tree)
+    for s in (2.0 ** -30, 0.25, 8.0, 2.0 ** 40):
+        assert same_bits(P.bidiagonal_values(d * s, e * s, backend=be_tree), v * s)
+
+
+# ---- stage 2: chase on the reference band ----------------------------------
+
+@pytest.mark.parametrize("name", golden_names("pipe_"))
+def test_chase_on_reference_band(P, be_tree, oracle, name):
+    g = load_golden(name)
+    ts = int(g["ts"])
+    d, e = P.band_to_bidiagonal(g["band"], ts, backend=be_tree)
+    vals = oracle.bidiagonal_values(d, e)[: g["vals"].size]
+    assert_close(vals, g["vals"], g["a"].dtype, g["band"].shape[0], what=name)
+
+
+# ---- full pipeline -----------------------------------------------------------
+
+@pytest.mark.parametrize("algo", ["tree", "faithful"])
+@pytest.mark.parametrize("name", golden_names("pipe_"))
+def test_pipeline_vs_reference(P, be_tree, be_faithful, name, algo):
+    g = load_golden(name)
+    be = be_tree if algo == "tree" else be_faithful
+    ts = int(g["ts"])
+    got = P.svdvals(g["a"], P.KernelConfig(tilesize=ts), backend=be)
+    assert got.dtype == g["vals"].dtype
+    assert got.shape == g["vals"].shape
+    assert np.all(got >= 0) and np.all(np.diff(got) <= 0)
+    if "sigma" in g:
+        assert_close(got, g["sigma"], g["a"].dtype, g["a"].shape[0], what=name + " vs sigma")
+    if np.max(np.abs(g["vals"])) == 0:
+        assert np.all(got == 0)
+        return
+    assert_close(got, g["vals"], g["a"].dtype, g["a"].shape[0], what=name)
+
+
+def test_reference_known_answers(P, be_tree):
+    assert np.array_equal(P.svdvals(np.diag([3.0, 2.0, 1.0]), backend=be_tree), [3.0, 2.0, 1.0])
+    got = P.svdvals(np.array([[0.0, 1.0], [1.0, 0.0]]), backend=be_tree)
+    assert np.allclose(got, [1.0, 1.0], rtol=4 * 2.0 ** -52)
+    assert np.all(P.svdvals(np.zeros((16, 16)), backend=be_tree) == 0)
+    assert np.allclose(P.svdvals(np.eye(16), backend=be_tree), 1.0, rtol=4 * 2.0 ** -52, atol=0)
+
+
+def test_scaling_equivariance_bitwise(P, be_tree):
+    a = np.random.default_rng(10).standard_normal((24, 24))
+    base = P.svdvals(a, backend=be_tree)
+    assert same_bits(P.svdvals(4.0 * a, backend=be_tree), 4.0 * base)
+
+
+def test_errors(P, be_tree):
+    with pytest.raises(P.ShapeError):
+        P.svdvals(np.zeros((3, 4)), backend=be_tree)
+    a = np.eye(4)
+    a[1, 1] = np.nan
+    with pytest.raises(P.ValidationError):
+        P.svdvals(a, backend=be_tree)
+    a[1, 1] = np.inf
+    with pytest.raises(P.ValidationError):
+        P.svdvals(a, backend=be_tree)
+
+
+@pytest.mark.parametrize("n", [1, 3, 5, 9, 13])
+def test_padding_count(P, be_tree, oracle, n):
+    a = np.random.default_rng(12).standard_normal((n, n))
+    got = P.svdvals(a, P.KernelConfig(tilesize=4), backend=be_tree)
+    assert got.shape == (n,)
+    assert_close(got, oracle.svdvals(a, 4), np.float64, n)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.float16])
+@pytest.mark.parametrize("n,ts", [(256, 32), (300, 64), (512, 128), (1024, 32)])
+def test_random_vs_oracle(P, be_tree, oracle, dtype, n, ts):
+    a = np.random.default_rng(n + ts).standard_normal((n, n)).astype(dtype)
+    got = P.svdvals(a, P.KernelConfig(tilesize=ts), backend=be_tree)
+    want = oracle.svdvals(a, ts)
+    assert_close(got, want, dtype, n, what=f"n={n} ts={ts} {np.dtype(dtype).name}")
+
+
+def test_batched_matches_single(P, be_tree):
+    import torch
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((6, 64, 64)).astype(np.float32)
+    got = P.svdvals_batched(a, P.KernelConfig(tilesize=16), backend=be_tree)
+    for i in range(a.shape[0]):
+        # batched reads row-major matrices as their transposes: same values
+        one = P.svdvals(torch.from_numpy(a[i]).cuda(), P.KernelConfig(tilesize=16), backend=be_tree)
+        assert np.array_equal(got[i], one.cpu().numpy())
+
+
+def test_device_tensor_path(P, be_tree):
+    import torch
+    a = torch.randn(200, 200, dtype=torch.float64, device="cuda")
+    got = P.svdvals(a, backend=be_tree)
+    assert got.is_cuda and got.dtype == torch.float64
+    want = torch.linalg.svdvals(a.cpu())
+    assert_close(got.cpu().numpy(), want.numpy(), np.float64, 200)
+
+
+def test_timers(P, be_tree):
+    timers = {}
+    P.svdvals(np.random.default_rng(0).standard_normal((256, 256)), backend=be_tree, timers=timers)
+    assert set(timers) == set(P.PHASE_KEYS)
+    assert all(v > 0 for v in timers.values())
