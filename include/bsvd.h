@@ -79,6 +79,9 @@ int32_t bsvd_default_tilesize(int64_t n);
 void bsvd_default_options(bsvd_options *opt);
 const char *bsvd_last_error(void);
 const char *bsvd_version(void);
+/* Number of CUDA kernels this library has launched in this process (all
+ * streams, all calls) -- the benchmark's launch-count evidence. */
+uint64_t bsvd_launch_counter(void);
 
 /* ---- whole path: secondstage.py:510-542 svdvals ------------------------ */
 

@@ -26,7 +26,7 @@ EXPORTS = (
     "bsvd_last_error", "bsvd_version", "bsvd_workspace_bytes", "bsvd_svdvals",
     "bsvd_svdvals_ex", "bsvd_svdvals_batched", "bsvd_banddiag",
     "bsvd_band_to_bidiagonal", "bsvd_bidiagonal_values", "bsvd_geqrt",
-    "bsvd_tsqrt_chain", "bsvd_unmqr", "bsvd_tsmqr_fused",
+    "bsvd_tsqrt_chain", "bsvd_unmqr", "bsvd_tsmqr_fused", "bsvd_launch_counter",
 )
 
 
@@ -65,6 +65,7 @@ def load(path: str = LIB_PATH):
         "bsvd_default_options": (None, [optp]),
         "bsvd_last_error": (ctypes.c_char_p, []),
         "bsvd_version": (ctypes.c_char_p, []),
+        "bsvd_launch_counter": (ctypes.c_uint64, []),
         "bsvd_workspace_bytes": (sz, [i32, i64, i64, cfgp]),
         "bsvd_svdvals": (i32, [vp, i32, i64, i64, cfgp, vp, vp, sz, vp, timp]),
         "bsvd_svdvals_ex": (i32, [vp, i32, i64, i64, cfgp, optp, vp, vp, sz, vp, timp]),

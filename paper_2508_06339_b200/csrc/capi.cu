@@ -11,9 +11,13 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <atomic>
+
 static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
 
 namespace bsvd_host {
+void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 bsvd_status set_error(bsvd_status st, const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
@@ -231,6 +235,7 @@ bsvd_status run(const void *a, bsvd_dtype dtype, int64_t n, int64_t lda, int64_t
 extern "C" {
 
 const char *bsvd_last_error(void) { return g_err; }
+uint64_t bsvd_launch_counter(void) { return g_launches.load(std::memory_order_relaxed); }
 const char *bsvd_version(void) { return "bsvd-b200 0.1.0 (sm_100a)"; }
 
 bsvd_status bsvd_validate_config(const bsvd_config *cfg) {

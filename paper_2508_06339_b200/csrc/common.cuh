@@ -67,8 +67,10 @@ __device__ __forceinline__ void reflector_scalars(C piv, C sigma, C aik, C rho, 
 
 }  // namespace bsvd
 
-// Host-side error plumbing (capi.cu owns the thread-local message).
+// Host-side error plumbing (capi.cu owns the thread-local message) and the
+// process-wide count of kernels this library has launched (bench evidence).
 namespace bsvd_host {
+void count_launch(unsigned n = 1);
 bsvd_status set_error(bsvd_status st, const char *fmt, ...);
 bsvd_status cuda_error(cudaError_t e, const char *where);
 }  // namespace bsvd_host

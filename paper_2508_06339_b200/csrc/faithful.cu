@@ -180,6 +180,7 @@ cudaError_t launch_geqrt_faithful(S *a, int64_t rs, int64_t cs, int ts, C *tau, 
                                   int64_t a_bstride, int64_t tau_bstride, cudaStream_t st) {
     k_geqrt_faithful<S, C><<<dim3(1, (unsigned)batch), ts, 0, st>>>(a, rs, cs, a_bstride, ts, tau,
                                                                     tau_bstride);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 
@@ -188,6 +189,7 @@ cudaError_t launch_tsqrt_faithful(S *r, int64_t rs, int64_t cs, TS_ bs, TA_ taus
                                   cudaStream_t st) {
     if (nb <= 0) return cudaSuccess;
     k_tsqrt_faithful<S, C, TS_, TA_><<<1, ts, 0, st>>>(r, rs, cs, bs, taus, nb, ts);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 
@@ -198,6 +200,7 @@ cudaError_t launch_unmqr_faithful(const S *panel, int64_t prs, int64_t pcs, cons
     if (ncols <= 0) return cudaSuccess;
     k_unmqr_faithful<S, C><<<(unsigned)(ncols / cpb), cpb, 0, st>>>(panel, prs, pcs, tau, x, xrs,
                                                                     xcs, ts, cpb);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 
@@ -207,6 +210,7 @@ cudaError_t launch_tsmqr_faithful(S *y, int64_t rs, int64_t cs, TS_ xs, TS_ vs, 
     if (nb <= 0 || ncols <= 0) return cudaSuccess;
     k_tsmqr_faithful<S, C, TS_, TA_><<<(unsigned)(ncols / cpb), cpb, 0, st>>>(y, rs, cs, xs, vs,
                                                                               taus, nb, ts, cpb);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 

@@ -28,6 +28,8 @@
 //                          X_bot -= U W
 //                 Each product is a register-blocked FMA GEMM (K = ts) with
 //                 the ts x ts operand streamed through shared memory.
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -55,7 +57,7 @@ __host__ __device__ inline int64_t tree_offset(int64_t m, int j) { // first slot
 }
 
 // Workspace of one sweep side for one matrix:
-//   node slots (<= 2N): Vk | Um | Tt   (3 ts^2 C each)
+//   node slots (tree_slots(N)): Vk | Um | Tt   (3 ts^2 C each)
 //   R slots (N): ts^2 C each
 //   arrival counters (N ints)
 template <typename C>
@@ -69,10 +71,13 @@ struct TreeWs {
     __host__ __device__ C *Tt(int64_t s) const { return nodes + s * 3 * ts2 + 2 * ts2; }
 };
 
+// sum_j ceil(m / 2^j) can exceed 2m (m = 5: 5+3+2+1 = 11): budget 2N + 64.
+__host__ __device__ inline int64_t tree_slots(int64_t N) { return 2 * N + 64; }
+
 template <typename C>
 __host__ __device__ inline size_t tree_ws_elems(int64_t N, int ts) {
     const int64_t ts2 = (int64_t)ts * ts;
-    return (size_t)(2 * N * 3 * ts2 + N * ts2) + (size_t)(N + 64) * sizeof(int) / sizeof(C) + 64;
+    return (size_t)(tree_slots(N) * 3 * ts2 + N * ts2) + (size_t)(N + 64) * sizeof(int) / sizeof(C) + 64;
 }
 
 template <typename C>
@@ -89,15 +94,33 @@ __device__ __forceinline__ C group_sum(C v) {   // sum over G consecutive lanes
     return v;
 }
 
+// Scale-invariant Householder scalars (LAPACK dlarfg convention): the
+// column (alpha, tail) with ||tail||^2 = sig maps to (beta, 0) with
+// H = I - tau v v^T, v = (1, tail*scale).  A zero tail gives tau = 0 (H = I).
+// Unlike the reference's absolute 10*eps guard (kernels.py:109)
+// this commutes with scaling, so tiny-scaled inputs keep full accuracy; the
+// faithful path (faithful.cu) keeps the reference's guard bit-for-bit.
+template <typename C>
+__device__ __forceinline__ void house_scalars(C alpha, C sig, C &beta, C &tau, C &scale) {
+    if (sig == C(0)) {
+        beta = alpha;
+        tau = C(0);
+        scale = C(1);
+    } else {
+        beta = -copysign(dsqrt(alpha * alpha + sig), alpha);
+        tau = (beta - alpha) / beta;
+        scale = C(1) / (alpha - beta);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Leaf: Householder QR of one ts x ts tile held column-major in smem (ld =
 // ts+1), reference reflector scalars.  Afterwards: R in the upper triangle,
-// v (unit implied) strictly below, tau[] in smem.
+// v (unit implied) strictly below, tau[] in smem (house_scalars).
 template <typename C, int TS>
 __device__ void leaf_qr(C *A, C *tau, C *scal) {
     constexpr int LD = TS + 1;
     constexpr int TPC = (kNT / TS) < 32 ? (kNT / TS) : 32;   // threads per column
-    const C two = C(2), eps10 = C(10) * Eps<C>::v;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int kk = 0; kk < TS - 1; ++kk) {
         if (warp == 0) {
@@ -105,11 +128,11 @@ __device__ void leaf_qr(C *A, C *tau, C *scal) {
             for (int r = kk + 1 + lane; r < TS; r += 32) sig += A[kk * LD + r] * A[kk * LD + r];
             sig = warp_sum_t(sig);
             const C alpha = A[kk * LD + kk];
-            C x, t, rhop;
-            reflector_scalars(alpha, sig, alpha, sig, eps10, two, x, t, rhop);
-            for (int r = kk + 1 + lane; r < TS; r += 32) A[kk * LD + r] = A[kk * LD + r] / x;
+            C beta, t, scale;
+            house_scalars(alpha, sig, beta, t, scale);
+            for (int r = kk + 1 + lane; r < TS; r += 32) A[kk * LD + r] *= scale;
             if (lane == 0) {
-                A[kk * LD + kk] = alpha - rhop;
+                A[kk * LD + kk] = beta;
                 tau[kk] = t;
             }
         }
@@ -162,10 +185,9 @@ __device__ void build_T(const C *tau, C *tmp, GetG getG, TGet tget, TSet tset) {
 __host__ __device__ __forceinline__ int pk(int r, int c) { return c * (c + 1) / 2 + r; }
 
 // TT-QR of [R_top; R_bot], both upper triangular, packed in smem.  After:
-// R_top updated, R_bot holds V_b (upper), tau[].  Reference TSQRT scalars.
+// R_top updated, R_bot holds V_b (upper), tau[] (house_scalars).
 template <typename C, int TS>
 __device__ void tt_qr(C *Rt, C *Rb, C *tau, C *scal) {
-    const C two = C(2), eps10 = C(10) * Eps<C>::v;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int kk = 0; kk < TS; ++kk) {
         if (warp == 0) {
@@ -173,11 +195,11 @@ __device__ void tt_qr(C *Rt, C *Rb, C *tau, C *scal) {
             for (int r = lane; r <= kk; r += 32) sig += Rb[pk(r, kk)] * Rb[pk(r, kk)];
             sig = warp_sum_t(sig);
             const C alpha = Rt[pk(kk, kk)];
-            C x, t, rhop;
-            reflector_scalars(alpha, sig, alpha, sig, eps10, two, x, t, rhop);
-            for (int r = lane; r <= kk; r += 32) Rb[pk(r, kk)] = Rb[pk(r, kk)] / x;
+            C beta, t, scale;
+            house_scalars(alpha, sig, beta, t, scale);
+            for (int r = lane; r <= kk; r += 32) Rb[pk(r, kk)] *= scale;
             if (lane == 0) {
-                Rt[pk(kk, kk)] = alpha - rhop;
+                Rt[pk(kk, kk)] = beta;
                 tau[kk] = t;
             }
         }
@@ -594,7 +616,7 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
     const int64_t ts2 = (int64_t)TS * TS;
     TreeWs<C> ws;
     ws.nodes = (C *)wsp;
-    ws.R = ws.nodes + 2 * N * 3 * ts2;
+    ws.R = ws.nodes + tree_slots(N) * 3 * ts2;
     ws.cnt = (int *)(ws.R + N * ts2);
     ws.ts2 = ts2;
     cudaError_t err;
@@ -619,43 +641,65 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
         tsm_set = tsm;
     }
     constexpr int CB = TileCfg<C>::elems / TS;
+    // Per-phase timing: three events per sweep side, recorded on the launch
+    // stream and read once at the end (no per-side host sync).
+    const bool timed = ev_p != nullptr;
+    (void)ev_t;
+    std::vector<cudaEvent_t> evs;
+    auto ev = [&]() -> cudaEvent_t {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        evs.push_back(e);
+        cudaEventRecord(e, st);
+        return e;
+    };
+    struct Mark { cudaEvent_t a, b, c; };
+    std::vector<Mark> marks;
     auto side = [&](int64_t k, bool lq) -> cudaError_t {
         View<S> V{a, lq ? n : 1, lq ? 1 : n};
         const int64_t top = lq ? k + 1 : k;
         if (top >= N) return cudaSuccess;
         const int64_t m = N - top;
         const int64_t ntrail = N - 1 - k;
-        if (ev_p) cudaEventRecord(ev_p[0], st);
+        Mark mk{};
+        if (timed) mk.a = ev();
         k_panel_tree<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
             V, m, top, k, ws, ws_elems, a_bstride);
+        bsvd_host::count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        if (ev_p) {
-            cudaEventRecord(ev_p[1], st);
-        }
+        if (timed) mk.b = ev();
         if (ntrail > 0) {
             const int64_t ncols = ntrail * TS;
             k_trail_tree<S, C, TS><<<dim3((unsigned)((ncols + CB - 1) / CB), (unsigned)batch), kNT, tsm, st>>>(
                 V, m, top, k, ncols, ws, ws_elems, a_bstride);
+            bsvd_host::count_launch();
             e = cudaGetLastError();
             if (e != cudaSuccess) return e;
         }
-        if (ev_p) {
-            cudaEventRecord(ev_t[1], st);
-            cudaEventSynchronize(ev_t[1]);
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev_p[0], ev_p[1]);
-            *pms += ms;
-            cudaEventElapsedTime(&ms, ev_p[1], ev_t[1]);
-            *tms += ms;
+        if (timed) {
+            mk.c = ev();
+            marks.push_back(mk);
         }
         return cudaSuccess;
     };
-    for (int64_t k = 0; k < N - 1; ++k) {
-        if ((err = side(k, false)) != cudaSuccess) return err;
-        if ((err = side(k, true)) != cudaSuccess) return err;
+    for (int64_t k = 0; k < N - 1 && err == cudaSuccess; ++k) {
+        if ((err = side(k, false)) != cudaSuccess) break;
+        err = side(k, true);
     }
-    return side(N - 1, false);
+    if (err == cudaSuccess) err = side(N - 1, false);
+    if (timed && !evs.empty()) {
+        cudaEventSynchronize(evs.back());
+        for (const Mark &mk : marks) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, mk.a, mk.b);
+            *pms += ms;
+            cudaEventElapsedTime(&ms, mk.b, mk.c);
+            *tms += ms;
+        }
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    }
+    return err;
 }
 
 template <typename S, typename C>

@@ -244,6 +244,7 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         const int64_t total = n * (int64_t)(bw + 1);
         dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 4096), (unsigned)batch);
         k_pack_band<S><<<grid, 256, 0, st>>>(a, n, lda, a_bstride, bw, band, ld, b);
+        bsvd_host::count_launch();
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
     if (n > 2) {
@@ -257,10 +258,12 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         int b_ = b;
         void *args[] = {&band, &n_, &b_, &ld_, &batch_, &progress, &nitems};
         err = cudaLaunchCooperativeKernel((void *)k_chase, dim3((unsigned)grid), dim3(256), args, 0, st);
+        bsvd_host::count_launch();
         if (err != cudaSuccess) return err;
     }
     dim3 g2((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch);
     k_extract_bidiag<<<g2, 256, 0, st>>>(band, n, ld, b, d, e);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 

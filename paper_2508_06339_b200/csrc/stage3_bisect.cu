@@ -125,10 +125,12 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
     double *o2 = (double *)ws;
     double *scal = o2 + batch * (2 * n - 1);
     k_bisect_prep<<<(unsigned)batch, 256, 0, st>>>(d, e, n, o2, scal);
+    bsvd_host::count_launch();
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     dim3 grid((unsigned)((n_out + 127) / 128), (unsigned)batch);
     k_bisect<OutT><<<grid, 128, 0, st>>>(o2, scal, n, n_out, out, out_stride);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 

@@ -38,6 +38,7 @@ cudaError_t copy_in_pad(const S *src, int64_t n, int64_t lda, int64_t src_bstrid
     const int64_t total = np * np;
     dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 8192), (unsigned)batch);
     k_copy_in_pad<S><<<grid, 256, 0, st>>>(src, n, lda, src_bstride, dst, np, nonfinite_flag);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 
@@ -57,6 +58,7 @@ template <typename S>
 cudaError_t clear_outside_band(S *a, int64_t n, int bw, int64_t batch, cudaStream_t st) {
     dim3 grid((unsigned)std::min<int64_t>((n * n + 255) / 256, 8192), (unsigned)batch);
     k_clear_outside_band<S><<<grid, 256, 0, st>>>(a, n, bw);
+    bsvd_host::count_launch();
     return cudaGetLastError();
 }
 

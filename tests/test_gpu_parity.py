@@ -122,6 +122,15 @@ def test_pipeline_vs_reference(P, be_tree, be_faithful, name, algo):
     assert np.all(got >= 0) and np.all(np.diff(got) <= 0)
     if "sigma" in g:
         assert_close(got, g["sigma"], g["a"].dtype, g["a"].shape[0], what=name + " vs sigma")
+    if algo == "tree" and "scaled" in name:
+        # The reference's absolute 10*eps reflector guard (kernels.py:109,
+        # SURVEY.md A1) makes its values on tiny-scaled input scale-dependent
+        # garbage; the faithful path reproduces them bit-for-bit (checked
+        # below), the tree path uses scale-invariant reflectors and must
+        # match the true singular values of the stored input instead.
+        want = np.linalg.svd(g["a"].astype(np.float64), compute_uv=False).astype(got.dtype)
+        assert_close(got, want, g["a"].dtype, g["a"].shape[0], what=name + " vs LAPACK")
+        return
     if np.max(np.abs(g["vals"])) == 0:
         assert np.all(got == 0)
         return
@@ -163,7 +172,8 @@ def test_padding_count(P, be_tree, oracle, n):
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32, np.float16])
-@pytest.mark.parametrize("n,ts", [(256, 32), (300, 64), (512, 128), (1024, 32)])
+@pytest.mark.parametrize("n,ts", [(256, 32), (300, 64), (300, 32), (320, 64), (512, 128),
+                                  (1000, 128), (1024, 32), (200, 8), (100, 4)])
 def test_random_vs_oracle(P, be_tree, oracle, dtype, n, ts):
     a = np.random.default_rng(n + ts).standard_normal((n, n)).astype(dtype)
     got = P.svdvals(a, P.KernelConfig(tilesize=ts), backend=be_tree)
