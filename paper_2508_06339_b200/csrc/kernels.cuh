@@ -43,6 +43,12 @@ cudaError_t banddiag_tree(S *a, int64_t n, int ts, int64_t batch, int64_t a_bstr
                           cudaStream_t st, cudaEvent_t *ev_panel, cudaEvent_t *ev_trail,
                           double *panel_ms, double *trail_ms);
 
+// ---- stage1_apply.cu (per-level WY trailing updates, ts >= 16) ----------
+template <typename S, typename C, int TS>
+cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
+                                int64_t top, int64_t k, int64_t m, const C *nodes,
+                                int64_t ws_bstride, cudaStream_t st);
+
 // ---- stage2_chase.cu -------------------------------------------------------
 size_t chase_workspace_bytes(int64_t n, int bw, int64_t batch);
 // Upper band (column-major padded n x n in S, band width bw) -> d, e (fp64).

@@ -1,0 +1,323 @@
+// stage1_apply.cu -- WY trailing updates of the tree stage 1, one launch per
+// tree level (the reference's UNMQR / TSMQR, kernels.py:364-421, in
+// compact-WY form):
+//
+//   leaf level  (every panel tile row l, in parallel):
+//       W = V_l^T X_l ;  X_l -= U_l W                      (U = V T^T)
+//   tree level j (every node with two children, in parallel):
+//       W = X_top + Vb^T X_bot ;  X_top -= T^T W ;  X_bot -= U W
+//
+// Grid = (column blocks) x (tile rows or node pairs) x (batch): thousands of
+// CTAs per launch instead of one CTA per column block walking the tree.
+// Each product is a BM x BN x K (= ts x BN x ts) register-blocked FMA GEMM:
+// the ts x ts operand is streamed through shared memory in K-chunks with
+// cp.async double buffering, the X / W tiles sit in shared memory, and the
+// warp layout (4 x 8 or 8 x 4 lanes, 8x4 / 4x4 per thread) keeps shared
+// traffic at <= 3 wavefronts per 32-lane FMA instruction group.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace bsvd {
+
+namespace apply {
+
+constexpr int kNT = 256;
+
+// Geometry per (compute type, ts).  BM = ts rows, BN columns per CTA.
+template <typename C, int TS> struct Geo;
+// fp32 / fp16-storage: 16 KiB... 32 KiB tiles, 8x4 per thread
+template <int TS> struct Geo<float, TS> {
+    static constexpr int BM = TS;
+    static constexpr int BN = 8192 / TS;               // ts*BN = 8192 elements
+    static constexpr int WGM = TS >= 128 ? 4 : (TS >= 64 ? 2 : 1);
+    static constexpr int WGN = 8 / WGM;
+    static constexpr int LM = TS >= 32 ? 4 : 2;
+    static constexpr int LN = 32 / LM;
+    static constexpr int MR = BM / (WGM * LM);
+    static constexpr int NR = BN / (WGN * LN);
+    static constexpr int KC = 32;
+};
+template <int TS> struct Geo<double, TS> {
+    static constexpr int BM = TS;
+    static constexpr int BN = 4096 / TS;
+    static constexpr int WGM = TS >= 128 ? 4 : (TS >= 64 ? 2 : 1);
+    static constexpr int WGN = 8 / WGM;
+    static constexpr int LM = TS >= 32 ? 8 : 4;
+    static constexpr int LN = 32 / LM;
+    static constexpr int MR = BM / (WGM * LM);
+    static constexpr int NR = BN / (WGN * LN);
+    static constexpr int KC = 16;
+};
+
+template <typename C> struct Vec;
+template <> struct Vec<float> { using t4 = float4; };
+template <> struct Vec<double> { using t4 = double2; };   // 16-byte granule
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Thread's microtile coordinates.
+template <typename G>
+struct Lane {
+    int m0, n0;
+    __device__ Lane() {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int wm = warp % G::WGM, wn = warp / G::WGM;
+        const int lm = lane % G::LM, ln = lane / G::LM;
+        m0 = wm * (G::BM / G::WGM) + lm * G::MR;
+        n0 = wn * (G::BN / G::WGN) + ln * G::NR;
+    }
+};
+
+// acc[i][j] += sign * sum_k A[k][m0+i] * Bs[k][n0+j]; A global [TS][TS] streamed
+// in KC-row chunks through Abuf (2 x KC x TS), Bs shared [TS][BNP].
+template <typename C, int TS, typename G, bool NEG, int BNP>
+__device__ __forceinline__ void gemm(const C *__restrict__ Ag, const C *Bs, C *Abuf,
+                                     C (&acc)[G::MR][G::NR], const Lane<G> &ln) {
+    constexpr int bnp = BNP;
+    constexpr int KC = (G::KC < TS) ? G::KC : TS;
+    constexpr int NCH = TS / KC;
+    constexpr int CH = KC * TS;                       // elements per chunk
+    constexpr int PER16 = 16 / (int)sizeof(C);        // elements per 16 B
+    constexpr int NV = CH / PER16;                    // 16 B granules per chunk
+    auto issue = [&](int ch) {
+        C *dst = Abuf + (ch & 1) * CH;
+        const C *src = Ag + (size_t)ch * CH;
+        for (int v = threadIdx.x; v < NV; v += kNT) cp_async16(dst + v * PER16, src + v * PER16);
+        cp_async_commit();
+    };
+    issue(0);
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+        if (ch + 1 < NCH) {
+            issue(ch + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const C *As = Abuf + (ch & 1) * CH;
+        const C *Bk = Bs + (size_t)ch * KC * bnp;
+#pragma unroll 4
+        for (int k = 0; k < KC; ++k) {
+            C a[G::MR], b[G::NR];
+#pragma unroll
+            for (int i = 0; i < G::MR; ++i) a[i] = As[k * TS + ln.m0 + i];
+#pragma unroll
+            for (int j = 0; j < G::NR; ++j) b[j] = Bk[k * bnp + ln.n0 + j];
+#pragma unroll
+            for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+                for (int j = 0; j < G::NR; ++j) {
+                    if (NEG) acc[i][j] -= a[i] * b[j];
+                    else acc[i][j] += a[i] * b[j];
+                }
+        }
+        __syncthreads();   // buffer (ch & 1) is refilled by issue(ch + 2)
+    }
+}
+
+template <typename S>
+struct View {
+    S *base;
+    int64_t rs, cs;
+    __device__ __forceinline__ S *ptr(int64_t r, int64_t c) const { return base + r * rs + c * cs; }
+};
+
+// X tile (TS rows from view row r0, BN columns from view column c0, columns
+// >= cmax masked) -> Xs[r][c] (row stride bnp).
+template <typename S, typename C, int TS, int BN>
+__device__ __forceinline__ void load_x(const View<S> &V, int64_t r0, int64_t c0, int64_t cmax,
+                                       C *Xs, int bnp) {
+    using CV = Conv<S, C>;
+    for (int idx = threadIdx.x; idx < TS * BN; idx += kNT) {
+        int r, c;
+        if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % BN; r = idx / BN; }
+        Xs[r * bnp + c] = (c0 + c < cmax) ? CV::ld(*V.ptr(r0 + r, c0 + c)) : C(0);
+    }
+}
+
+// Store the thread's microtile straight from registers.
+template <typename S, typename C, typename G>
+__device__ __forceinline__ void store_acc(const View<S> &V, int64_t r0, int64_t c0, int64_t cmax,
+                                          const C (&acc)[G::MR][G::NR], const Lane<G> &ln) {
+    using CV = Conv<S, C>;
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int j = 0; j < G::NR; ++j)
+            if (c0 + ln.n0 + j < cmax) *V.ptr(r0 + ln.m0 + i, c0 + ln.n0 + j) = CV::st(acc[i][j]);
+}
+
+template <typename C, typename G>
+__device__ __forceinline__ void init_from(C (&acc)[G::MR][G::NR], const C *Xs, int bnp,
+                                          const Lane<G> &ln) {
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int j = 0; j < G::NR; ++j) acc[i][j] = Xs[(ln.m0 + i) * bnp + ln.n0 + j];
+}
+
+template <typename C, typename G>
+__device__ __forceinline__ void zero(C (&acc)[G::MR][G::NR]) {
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int j = 0; j < G::NR; ++j) acc[i][j] = C(0);
+}
+
+template <typename C, typename G>
+__device__ __forceinline__ void to_smem(const C (&acc)[G::MR][G::NR], C *Ws, int bnp,
+                                        const Lane<G> &ln) {
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int j = 0; j < G::NR; ++j) Ws[(ln.m0 + i) * bnp + ln.n0 + j] = acc[i][j];
+}
+
+}  // namespace apply
+
+using namespace apply;
+
+// Leaf level: grid (column blocks, m tile rows, batch).
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(apply::kNT) k_apply_leaf(View<S> V, int64_t top, int64_t cbase,
+                                                           int64_t ncols, const C *nodes,
+                                                           int64_t ts2x3, int64_t ws_bstride,
+                                                           int64_t a_bstride) {
+    using G = Geo<C, TS>;
+    constexpr int BNP = G::BN + 16 / (int)sizeof(C);
+    constexpr int KC = (G::KC < TS) ? G::KC : TS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *Abuf = (C *)smem_raw;
+    C *Xs = Abuf + 2 * KC * TS;
+    C *Ws = Xs + TS * BNP;
+    const int64_t b = blockIdx.z, l = blockIdx.y;
+    V.base += b * a_bstride;
+    nodes += b * ws_bstride;
+    const C *Vk = nodes + l * ts2x3, *Um = Vk + (int64_t)TS * TS;
+    const int64_t c0 = cbase + (int64_t)blockIdx.x * G::BN, cmax = cbase + ncols;
+    const int64_t r0 = (top + l) * TS;
+    const Lane<G> ln;
+    load_x<S, C, TS, G::BN>(V, r0, c0, cmax, Xs, BNP);
+    __syncthreads();
+    C acc[G::MR][G::NR];
+    zero<C, G>(acc);
+    gemm<C, TS, G, false, BNP>(Vk, Xs, Abuf, acc, ln);   // W = V^T X
+    to_smem<C, G>(acc, Ws, BNP, ln);
+    init_from<C, G>(acc, Xs, BNP, ln);
+    __syncthreads();
+    gemm<C, TS, G, true, BNP>(Um, Ws, Abuf, acc, ln);    // X -= U W
+    store_acc<S, C, G>(V, r0, c0, cmax, acc, ln);
+}
+
+// Tree level j: grid (column blocks, node pairs, batch).  Node (j, p) combines
+// leaves a = (2p) << (j-1) (top) and bb = (2p+1) << (j-1) (bottom); its
+// reflector slot is slot0 + p.
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(apply::kNT) k_apply_tt(View<S> V, int64_t top, int64_t cbase,
+                                                         int64_t ncols, const C *nodes,
+                                                         int64_t ts2x3, int64_t slot0, int j,
+                                                         int64_t ws_bstride, int64_t a_bstride) {
+    using G = Geo<C, TS>;
+    constexpr int BNP = G::BN + 16 / (int)sizeof(C);
+    constexpr int KC = (G::KC < TS) ? G::KC : TS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *Abuf = (C *)smem_raw;
+    C *Xt = Abuf + 2 * KC * TS;
+    C *Xb = Xt + TS * BNP;
+    C *Ws = Xb + TS * BNP;
+    const int64_t b = blockIdx.z, p = blockIdx.y;
+    V.base += b * a_bstride;
+    nodes += b * ws_bstride;
+    const C *Vk = nodes + (slot0 + p) * ts2x3, *Um = Vk + (int64_t)TS * TS, *Tt = Um + (int64_t)TS * TS;
+    const int64_t c0 = cbase + (int64_t)blockIdx.x * G::BN, cmax = cbase + ncols;
+    const int64_t rt = (top + ((2 * p) << (j - 1))) * TS;
+    const int64_t rb = (top + ((2 * p + 1) << (j - 1))) * TS;
+    const Lane<G> ln;
+    load_x<S, C, TS, G::BN>(V, rt, c0, cmax, Xt, BNP);
+    load_x<S, C, TS, G::BN>(V, rb, c0, cmax, Xb, BNP);
+    __syncthreads();
+    C acc[G::MR][G::NR];
+    init_from<C, G>(acc, Xt, BNP, ln);
+    gemm<C, TS, G, false, BNP>(Vk, Xb, Abuf, acc, ln);   // W = X_top + Vb^T X_bot
+    to_smem<C, G>(acc, Ws, BNP, ln);
+    __syncthreads();
+    init_from<C, G>(acc, Xt, BNP, ln);
+    gemm<C, TS, G, true, BNP>(Tt, Ws, Abuf, acc, ln);    // X_top -= T^T W
+    store_acc<S, C, G>(V, rt, c0, cmax, acc, ln);
+    init_from<C, G>(acc, Xb, BNP, ln);
+    gemm<C, TS, G, true, BNP>(Um, Ws, Abuf, acc, ln);    // X_bot -= U W
+    store_acc<S, C, G>(V, rb, c0, cmax, acc, ln);
+}
+
+template <typename C, int TS>
+size_t apply_smem(bool tt) {
+    using G = Geo<C, TS>;
+    constexpr int BNP = G::BN + 16 / (int)sizeof(C);
+    constexpr int KC = (G::KC < TS) ? G::KC : TS;
+    return (size_t)(2 * KC * TS + (tt ? 3 : 2) * TS * BNP) * sizeof(C);
+}
+
+// Host side: one launch for the leaves, one per tree level.
+template <typename S, typename C, int TS>
+cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
+                                int64_t top, int64_t k, int64_t m, const C *nodes,
+                                int64_t ws_bstride, cudaStream_t st) {
+    using G = Geo<C, TS>;
+    const int64_t ncols = (n / TS - 1 - k) * TS;
+    if (ncols <= 0) return cudaSuccess;
+    View<S> V{a, lq ? n : 1, lq ? 1 : n};
+    const int64_t cbase = (k + 1) * TS;
+    const int64_t ts2x3 = 3 * (int64_t)TS * TS;
+    const unsigned gx = (unsigned)((ncols + G::BN - 1) / G::BN);
+    static size_t set_leaf = 0, set_tt = 0;
+    const size_t sl = apply_smem<C, TS>(false), stt = apply_smem<C, TS>(true);
+    cudaError_t e;
+    if (sl > set_leaf) {
+        if ((e = cudaFuncSetAttribute(k_apply_leaf<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sl)) != cudaSuccess) return e;
+        set_leaf = sl;
+    }
+    if (stt > set_tt) {
+        if ((e = cudaFuncSetAttribute(k_apply_tt<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stt)) != cudaSuccess) return e;
+        set_tt = stt;
+    }
+    k_apply_leaf<S, C, TS><<<dim3(gx, (unsigned)m, (unsigned)batch), apply::kNT, sl, st>>>(
+        V, top, cbase, ncols, nodes, ts2x3, ws_bstride, a_bstride);
+    bsvd_host::count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // tree levels: count(j) = ceil(m / 2^j); node (j, p) has two children iff 2p+1 < count(j-1)
+    int64_t off = 0, cnt_prev = m;
+    for (int j = 1; ((int64_t)1 << (j - 1)) < m; ++j) {
+        off += cnt_prev;                                   // tree_offset(m, j)
+        const int64_t cnt = (m + ((int64_t)1 << j) - 1) >> j;
+        const int64_t pairs = cnt_prev / 2;                // nodes with a right child
+        if (pairs > 0) {
+            k_apply_tt<S, C, TS><<<dim3(gx, (unsigned)pairs, (unsigned)batch), apply::kNT, stt, st>>>(
+                V, top, cbase, ncols, nodes, ts2x3, off, j, ws_bstride, a_bstride);
+            bsvd_host::count_launch();
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+        cnt_prev = cnt;
+    }
+    return cudaSuccess;
+}
+
+#define INST(S, C, TS)                                                                         \
+    template cudaError_t launch_apply_levels<S, C, TS>(S *, int64_t, int64_t, int64_t, bool,    \
+                                                       int64_t, int64_t, int64_t, const C *,    \
+                                                       int64_t, cudaStream_t);
+#define INST3(TS) INST(double, double, TS) INST(float, float, TS) INST(__half, float, TS)
+INST3(16)
+INST3(32)
+INST3(64)
+INST3(128)
+#undef INST3
+#undef INST
+
+}  // namespace bsvd

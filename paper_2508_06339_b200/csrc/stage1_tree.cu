@@ -670,11 +670,17 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
         if (e != cudaSuccess) return e;
         if (timed) mk.b = ev();
         if (ntrail > 0) {
-            const int64_t ncols = ntrail * TS;
-            k_trail_tree<S, C, TS><<<dim3((unsigned)((ncols + CB - 1) / CB), (unsigned)batch), kNT, tsm, st>>>(
-                V, m, top, k, ncols, ws, ws_elems, a_bstride);
-            bsvd_host::count_launch();
-            e = cudaGetLastError();
+            if constexpr (TS >= 16) {
+                // one launch per tree level, thousands of CTAs (stage1_apply.cu)
+                e = launch_apply_levels<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes,
+                                                  ws_elems, st);
+            } else {
+                const int64_t ncols = ntrail * TS;
+                k_trail_tree<S, C, TS><<<dim3((unsigned)((ncols + CB - 1) / CB), (unsigned)batch), kNT, tsm, st>>>(
+                    V, m, top, k, ncols, ws, ws_elems, a_bstride);
+                bsvd_host::count_launch();
+                e = cudaGetLastError();
+            }
             if (e != cudaSuccess) return e;
         }
         if (timed) {

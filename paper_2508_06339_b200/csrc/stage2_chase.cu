@@ -24,6 +24,10 @@
 // the bulges (r - c in [-2b, b]), 3b+1 doubles per column: 50 MB at
 // n = 16384, b = 128, i.e. L2-resident on B200 (126 MB L2).
 #include <cooperative_groups.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -64,18 +68,41 @@ __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Cluster helpers (CS CTAs of one thread-block cluster cooperate on an op).
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+template <int CS>
+__device__ __forceinline__ void cluster_sync() {
+    if constexpr (CS > 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                     "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        __syncthreads();
+    }
+}
+
 // Householder generation (LAPACK dlarfg convention): x -> beta e1 with
-// H = I - tau v v^T, v[0] = 1.  Executed by warp 0; v (len L) into vs.
-// Returns tau (0 when the tail is already zero: H = I).
-__device__ double make_reflector_warp(const Band &A, int64_t r0, int64_t c0, bool column, int L,
-                                      double *vs) {
+// H = I - tau v v^T, v[0] = 1.  Executed by warp 0 of every CTA of the
+// cluster (identical arithmetic -> identical v); v (len L) into vs.
+__device__ void make_reflector_warp(const Band &A, int64_t r0, int64_t c0, bool column, int L,
+                                    double *vs, double *tau_s, double *beta_s) {
     const int lane = threadIdx.x & 31;
-    double alpha = __ldcg(A.at(r0, c0));
+    const double alpha = __ldcg(A.at(r0, c0));
+    double x4[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = 1 + lane + 32 * q;
+        x4[q] = j < L ? (column ? __ldcg(A.at(r0 + j, c0)) : __ldcg(A.at(r0, c0 + j))) : 0.0;
+    }
     double sig = 0.0;
-    for (int j = 1 + lane; j < L; j += 32) {
-        const double xj = column ? __ldcg(A.at(r0 + j, c0)) : __ldcg(A.at(r0, c0 + j));
-        vs[j] = xj;
-        sig += xj * xj;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = 1 + lane + 32 * q;
+        if (j < L) vs[j] = x4[q];
+        sig += x4[q] * x4[q];
     }
     sig = warp_sum(sig);
     double tau = 0.0, scale = 0.0, beta = alpha;
@@ -85,107 +112,198 @@ __device__ double make_reflector_warp(const Band &A, int64_t r0, int64_t c0, boo
         scale = 1.0 / (alpha - beta);
     }
     __syncwarp();
-    for (int j = 1 + lane; j < L; j += 32) {
-        vs[j] = vs[j] * scale;
-        if (column) __stcg(A.at(r0 + j, c0), 0.0); else __stcg(A.at(r0, c0 + j), 0.0);
-    }
+    for (int j = 1 + lane; j < L; j += 32) vs[j] *= scale;
     if (lane == 0) {
         vs[0] = 1.0;
-        __stcg(A.at(r0, c0), beta);
-    }
-    return tau;
-}
-
-// Left op: pivot column p, rows [p, p+L), applied to columns (p, chi).
-__device__ void chase_left(const Band &A, int64_t p, int L, int64_t chi, double *vs,
-                           double *tau_s) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    if (warp == 0) {
-        const double t = make_reflector_warp(A, p, p, true, L, vs);
-        if (lane == 0) *tau_s = t;
-    }
-    __syncthreads();
-    const double tau = *tau_s;
-    if (tau == 0.0) return;
-    constexpr int kMaxPer = 4;   // L <= 128 rows -> <= 4 per lane
-    for (int64_t c = p + 1 + warp; c < chi; c += nw) {
-        double xv[kMaxPer];
-        double w = 0.0;
-#pragma unroll
-        for (int q = 0; q < kMaxPer; ++q) {
-            const int j = lane + 32 * q;
-            xv[q] = (j < L) ? __ldcg(A.at(p + j, c)) : 0.0;
-            if (j < L) w += vs[j] * xv[q];
-        }
-        w = warp_sum(w) * tau;
-#pragma unroll
-        for (int q = 0; q < kMaxPer; ++q) {
-            const int j = lane + 32 * q;
-            if (j < L) __stcg(A.at(p + j, c), xv[q] - w * vs[j]);
-        }
+        *tau_s = tau;
+        *beta_s = beta;
     }
 }
 
-// Right op: pivot row p, columns [c0, c0+L), applied to rows [rlo, rhi) \ {p}.
-__device__ void chase_right(const Band &A, int64_t p, int64_t c0, int L, int64_t rlo,
-                            int64_t rhi, double *vs, double *tau_s) {
+__device__ void write_pivot(const Band &A, int64_t r0, int64_t c0, bool column, int L, double beta) {
+    const int lane = threadIdx.x & 31;
+    for (int j = 1 + lane; j < L; j += 32) {
+        if (column) __stcg(A.at(r0 + j, c0), 0.0); else __stcg(A.at(r0, c0 + j), 0.0);
+    }
+    if (lane == 0) __stcg(A.at(r0, c0), beta);
+}
+
+// Left op slice: pivot column p (rows [p, p+L), L <= 128), this CTA's
+// columns [ca, cb) (<= 64).  Register tile: warp w owns columns w, w+8, ...;
+// lane l holds rows l, l+32, l+64, l+96 of each -- every load of the slice is
+// issued before the first use (one L2 round trip), no shared staging, no
+// per-element index division.
+__device__ void left_slice(const Band &A, int64_t p, int L, int64_t ca, int64_t cb,
+                           const double *vs, double tau) {
+    const int ncol = (int)(cb - ca);
+    if (ncol <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == 0) {
-        const double t = make_reflector_warp(A, p, c0, false, L, vs);
-        if (lane == 0) *tau_s = t;
+    constexpr int CPW = 8;                      // columns per warp (64 / 8 warps)
+    double x[CPW][4];
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = (lane + 32 * q < L) ? vs[lane + 32 * q] : 0.0;
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + 8 * k;
+        const double *col = (c < ncol) ? A.at(p, ca + c) : nullptr;   // rows contiguous
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = lane + 32 * q;
+            x[k][q] = (col && r < L) ? __ldcg(col + r) : 0.0;
+        }
     }
-    __syncthreads();
-    const double tau = *tau_s;
-    if (tau == 0.0) return;
-    for (int64_t r = rlo + threadIdx.x; r < rhi; r += blockDim.x) {
-        if (r == p) continue;
-        double w = 0.0;
-        for (int j = 0; j < L; ++j) w += __ldcg(A.at(r, c0 + j)) * vs[j];
-        w *= tau;
-        for (int j = 0; j < L; ++j) {
-            double *q = A.at(r, c0 + j);
-            __stcg(q, __ldcg(q) - w * vs[j]);
+    double w[CPW];
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        w[k] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[k] += v[q] * x[k][q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) w[k] += __shfl_xor_sync(0xffffffffu, w[k], o);
+#pragma unroll
+    for (int k = 0; k < CPW; ++k) {
+        const int c = warp + 8 * k;
+        if (c >= ncol) continue;
+        double *col = A.at(p, ca + c);
+        const double tw = tau * w[k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = lane + 32 * q;
+            if (r < L) __stcg(col + r, x[k][q] - tw * v[q]);
         }
     }
 }
 
+// Right op slice: pivot row p, columns [c0, c0+L) (L <= 128), this CTA's
+// rows [ra, rb) (<= 64).  Register tile: lanes <-> 32 consecutive rows
+// (coalesced column segments), warp w = (row half, column phase q of 4);
+// each thread holds columns q, q+4, ... of its row (<= 32 values); the four
+// column-phase partial dots are combined through shared memory.
+__device__ void right_slice(const Band &A, int64_t p, int64_t c0, int L, int64_t ra, int64_t rb,
+                            const double *vs, double tau, double *part) {
+    const int nrow = (int)(rb - ra);
+    if (nrow <= 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int half = warp & 1, q = warp >> 1;           // 2 row halves x 4 column phases
+    const int r = half * 32 + lane;
+    const bool act = r < nrow;
+    constexpr int JPT = 32;                             // columns per thread (128 / 4)
+    double x[JPT];
+    const double *base = A.at(ra + r, c0);              // column j at base + j*(ld-1)
+    const int64_t cstride = A.ld - 1;                   // (r, c+1) - (r, c)
+#pragma unroll
+    for (int k = 0; k < JPT; ++k) {
+        const int j = q + 4 * k;
+        x[k] = (act && j < L) ? __ldcg(base + (int64_t)j * cstride) : 0.0;
+    }
+    double w = 0.0;
+#pragma unroll
+    for (int k = 0; k < JPT; ++k) {
+        const int j = q + 4 * k;
+        if (j < L) w += x[k] * vs[j];
+    }
+    part[q * 64 + r] = w;
+    __syncthreads();
+    const double tw = tau * (part[r] + part[64 + r] + part[128 + r] + part[192 + r]);
+    if (act && ra + r != p) {
+        double *rowp = A.at(ra + r, c0);
+#pragma unroll
+        for (int k = 0; k < JPT; ++k) {
+            const int j = q + 4 * k;
+            if (j < L) __stcg(rowp + (int64_t)j * cstride, x[k] - tw * vs[j]);
+        }
+    }
+}
+
+// One op (index i) of sweep s.  All CTAs of the cluster call this with the
+// same arguments; rank `rk` of CS owns a contiguous slice of the op.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int CS>
+__device__ void chase_op(const Band &A, int64_t s, int i, int64_t n, int b, unsigned rk,
+                         double *vs, double *tau_s, double *beta_s, double *part,
+                         unsigned long long *tr) {
+    bool column;
+    int64_t p, c0, lo, hi;   // pivot row/col, first column, apply range [lo, hi)
+    int L;
+    if (i == 0) {                       // right op: annihilate row s
+        column = false; p = s; c0 = s + 1;
+        L = (int)(min(s + 1 + b, n) - c0);
+        lo = s; hi = min(s + 1 + b, n);
+    } else {
+        const int64_t t = (i - 1) / 2;
+        const int64_t r0 = s + 1 + t * b;
+        if (((i - 1) & 1) == 0) {       // left op: annihilate column r0
+            column = true; p = r0; c0 = r0;
+            L = (int)(min(r0 + b, n) - r0);
+            lo = r0 + 1; hi = min(r0 + 2 * b, n);
+        } else {                        // right op: annihilate row r0's fill
+            column = false; p = r0; c0 = r0 + b;
+            L = (int)(min(r0 + 2 * b, n) - c0);
+            lo = r0; hi = min(r0 + 2 * b, n);
+        }
+    }
+    if (L < 2) return;                  // uniform across the cluster
+    if ((threadIdx.x >> 5) == 0)
+        make_reflector_warp(A, column ? p : p, c0, column, L, vs, tau_s, beta_s);
+    __syncthreads();
+    if (tr && threadIdx.x == 0) tr[2] = gtimer();
+    cluster_sync<CS>();                 // every CTA has read the pivot
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
+    const double tau = *tau_s;
+    if (rk == 0 && (threadIdx.x >> 5) == 0) write_pivot(A, p, c0, column, L, *beta_s);
+    if (tau != 0.0) {
+        const int64_t tot = hi - lo;
+        const int64_t chunk = (tot + CS - 1) / CS;
+        const int64_t a = lo + (int64_t)rk * chunk, e = min(a + chunk, hi);
+        if (column) left_slice(A, p, L, a, e, vs, tau);
+        else right_slice(A, p, c0, L, a, e, vs, tau, part);
+    }
+    __syncthreads();
+    if (tr && threadIdx.x == 0) tr[4] = gtimer();
+    if (threadIdx.x == 0) __threadfence();   // publish this CTA's slice gpu-wide
+}
+
+template <int CS>
 __global__ void __launch_bounds__(256) k_chase(double *band, int64_t n, int b, int64_t ld,
-                                               int64_t batch, int *progress, int64_t nitems) {
+                                               int64_t batch, int *progress, int64_t nitems,
+                                               unsigned long long *trace) {
     __shared__ double vs[128];
-    __shared__ double tau_s;
-    for (int64_t w = blockIdx.x; w < nitems; w += gridDim.x) {
+    __shared__ double part[256];
+    __shared__ double tau_s, beta_s;
+    const unsigned rk = CS > 1 ? cluster_rank() : 0;
+    const int64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    for (int64_t w = cid; w < nitems; w += ncl) {
         const int64_t s = w / batch, m = w % batch;
         const Band A{band + m * n * ld, n, ld, b};
         int *prog = progress + m * n;
         const int nops = chase_nops(s, n, b);
         const int nprev = s > 0 ? chase_nops(s - 1, n, b) : 0;
         for (int i = 0; i < nops; ++i) {
+            unsigned long long *tr =
+                (trace && rk == 0 && m == 0 && s < 256 && i < 32) ? trace + (s * 32 + i) * 8 : nullptr;
+            if (tr && threadIdx.x == 0) tr[0] = gtimer();
             if (s > 0) {
                 if (threadIdx.x == 0) {
                     const int need = min(i + 4, nprev);
-                    while (ld_acquire(prog + s - 1) < need) __nanosleep(40);
+                    while (ld_acquire(prog + s - 1) < need) __nanosleep(32);
+                    __threadfence();
                 }
                 __syncthreads();
             }
-            if (i == 0) {
-                const int64_t chi = min(s + 1 + b, n);
-                if (chi - (s + 1) >= 2) chase_right(A, s, s + 1, (int)(chi - (s + 1)), s, chi, vs, &tau_s);
-            } else {
-                const int64_t t = (i - 1) / 2;
-                const int64_t r0 = s + 1 + t * b;
-                if (((i - 1) & 1) == 0) {
-                    const int64_t rhi = min(r0 + b, n);
-                    if (rhi - r0 >= 2) chase_left(A, r0, (int)(rhi - r0), min(r0 + 2 * b, n), vs, &tau_s);
-                } else {
-                    const int64_t c0 = r0 + b, c1 = min(r0 + 2 * b, n);
-                    if (c1 - c0 >= 2) chase_right(A, r0, c0, (int)(c1 - c0), r0, c1, vs, &tau_s);
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                st_release(prog + s, i + 1);
-            }
+            if (tr && threadIdx.x == 0) tr[1] = gtimer();
+            chase_op<CS>(A, s, i, n, b, rk, vs, &tau_s, &beta_s, part, tr);
+            cluster_sync<CS>();         // all slices of op i are written
+            if (rk == 0 && threadIdx.x == 0) st_release(prog + s, i + 1);
+            if (tr && threadIdx.x == 0) tr[5] = gtimer();
         }
     }
 }
@@ -248,18 +366,66 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
     if (n > 2) {
-        int dev = 0, nsm = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chase, 256, 0);
+        // Cluster size: a single large band splits every op over 4 CTAs (4x
+        // the L2 bandwidth per op); batches get their parallelism from the
+        // matrices.  Shared slice: b x ceil(2b/CS) doubles.
+        // Cluster size: every op is split over CS CTAs so each CTA's slice is
+        // <= 64 columns (left op) or <= 64 rows (right op) of a register tile.
+        const int CS = b > 64 ? 4 : (b > 32 ? 2 : 1);
+        const size_t smem = 0;
         int64_t nitems = (n - 2) * batch;   // sweeps 0..n-3 do work (reference loop bound)
-        int64_t grid = std::min<int64_t>(nitems, (int64_t)nsm * std::max(per_sm, 1));
+        // useful concurrency: a sweep trails its predecessor by 4 ops
+        int64_t nops0 = 1 + 2 * ((n - 2 + b) / b);
+        int64_t want = std::min<int64_t>(nitems, batch * (nops0 / 4 + 2));
+        cudaLaunchConfig_t lc{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        lc.blockDim = dim3(256);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = st;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        void (*kern)(double *, int64_t, int, int64_t, int64_t, int *, int64_t, unsigned long long *) =
+            CS == 4 ? k_chase<4> : (CS == 2 ? k_chase<2> : k_chase<1>);
+        if (CS > 1) {
+            int max_clusters = 0;
+            lc.gridDim = dim3((unsigned)(want * CS));
+            err = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &lc);
+            if (err != cudaSuccess) return err;
+            want = std::min<int64_t>(want, std::max(max_clusters, 1));
+        } else {
+            int dev = 0, nsm = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+            want = std::min<int64_t>(want, (int64_t)nsm * std::max(per_sm, 1));
+        }
+        lc.gridDim = dim3((unsigned)(want * CS));
         int64_t n_ = n, ld_ = ld, batch_ = batch;
         int b_ = b;
-        void *args[] = {&band, &n_, &b_, &ld_, &batch_, &progress, &nitems};
-        err = cudaLaunchCooperativeKernel((void *)k_chase, dim3((unsigned)grid), dim3(256), args, 0, st);
+        // BSVD_CHASE_TRACE=<file>: per-op phase timestamps of the first
+        // 256 sweeps (development instrumentation, off by default).
+        const char *trace_path = getenv("BSVD_CHASE_TRACE");
+        unsigned long long *trace = nullptr;
+        const size_t trace_bytes = 256 * 32 * 8 * sizeof(unsigned long long);
+        if (trace_path) {
+            cudaMallocAsync((void **)&trace, trace_bytes, st);
+            cudaMemsetAsync(trace, 0, trace_bytes, st);
+        }
+        err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, progress, nitems, trace);
         bsvd_host::count_launch();
         if (err != cudaSuccess) return err;
+        if (trace) {
+            std::vector<unsigned long long> h(trace_bytes / 8);
+            cudaMemcpyAsync(h.data(), trace, trace_bytes, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            FILE *f = fopen(trace_path, "wb");
+            if (f) { fwrite(h.data(), 1, trace_bytes, f); fclose(f); }
+            cudaFreeAsync(trace, st);
+        }
     }
     dim3 g2((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch);
     k_extract_bidiag<<<g2, 256, 0, st>>>(band, n, ld, b, d, e);
