@@ -28,6 +28,9 @@
 //                          X_bot -= U W
 //                 Each product is a register-blocked FMA GEMM (K = ts) with
 //                 the ts x ts operand streamed through shared memory.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <vector>
 
 #include "common.cuh"
@@ -225,6 +228,19 @@ __device__ void tt_qr(C *Rt, C *Rb, C *tau, C *scal) {
     (void)scal;
 }
 
+}  // namespace bsvd
+#include "panel_qr.cuh"
+namespace bsvd {
+
+// Development instrumentation (BSVD_PANEL_TRACE): leaf-phase timestamps of
+// one chosen panel launch.
+__device__ unsigned long long *g_panel_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // View helpers: tile (tr, tc) of the (possibly transposed) matrix view.
 template <typename S>
 struct View {
@@ -259,10 +275,16 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
     const int64_t l = blockIdx.x;
     const int tid = threadIdx.x;
     const int64_t ts2 = (int64_t)TS * TS;
+    auto house = [](C a, C s, C &b, C &t, C &sc) { house_scalars(a, s, b, t, sc); };
+    unsigned long long *trc = g_panel_trace && b == 0 && l < 64 ? g_panel_trace + l * 8 : nullptr;
+    auto mark = [&](int ph) {
+        if (trc && tid == 0) trc[ph] = gtimer_ns();
+    };
 
     // ---- leaf: GEQRT of view tile (top + l, k) ----
     {
         C *A = sm;
+        mark(0);
         const int64_t r0 = (top + l) * TS, c0 = k * TS;
         for (int idx = tid; idx < TS * TS; idx += kNT) {
             int r, c;
@@ -270,7 +292,9 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
             A[c * LD + r] = CV::ld(*V.ptr(r0 + r, c0 + c));
         }
         __syncthreads();
-        leaf_qr<C, TS>(A, tau, scal);
+        mark(1);
+        panel::leaf_qr_la<C, TS, kNT>(A, tau, house);
+        mark(2);
         // R -> ws.R[l] (column-major, upper triangle + zeros)
         C *Rg = ws.R + l * ts2;
         for (int idx = tid; idx < TS * TS; idx += kNT) {
@@ -282,16 +306,21 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
         for (int idx = tid; idx < TS * TS; idx += kNT) {
             const int j = idx / TS, i = idx % TS;
             if (i < j) {
-                C s = A[i * LD + j];   // V[j][i]
-                for (int r = j + 1; r < TS; ++r) s += A[i * LD + r] * A[j * LD + r];
-                A[j * LD + i] = s;
+                const C *vi = A + i * LD, *vj = A + j * LD;
+                C s0 = vi[j], s1 = C(0);   // V[j][i] (V[j][j] = 1)
+                int r = j + 1;
+                for (; r + 1 < TS; r += 2) {
+                    s0 += vi[r] * vj[r];
+                    s1 += vi[r + 1] * vj[r + 1];
+                }
+                if (r < TS) s0 += vi[r] * vj[r];
+                A[j * LD + i] = s0 + s1;
             }
         }
         __syncthreads();
-        build_T<C, TS>(tau, tmp,
-                       [&](int i, int j) { return A[j * LD + i]; },
-                       [&](int i, int j) { return A[j * LD + i]; },
-                       [&](int i, int j, C v) { A[j * LD + i] = v; });
+        mark(3);
+        panel::build_T_rec<C, TS, kNT>(tau, A + TS * LD, [&](int i, int j) -> C & { return A[j * LD + i]; });
+        mark(4);
         // Vk[r][i] = V(r, i);  Um[i][r] = U(r, i) = sum_{j=i..r} V(r,j) T(i,j)
         C *Vk = ws.Vk(l), *Um = ws.Um(l);
         for (int idx = tid; idx < TS * TS; idx += kNT) {
@@ -300,13 +329,20 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
         }
         for (int idx = tid; idx < TS * TS; idx += kNT) {
             const int i = idx / TS, r = idx % TS;
-            C s = C(0);
+            C s0 = C(0), s1 = C(0);
             if (r >= i) {
-                s = A[i * LD + i] * ((r == i) ? C(1) : A[i * LD + r]);   // j = i: T(i,i)=tau_i
-                for (int j = i + 1; j <= r; ++j) s += ((j == r) ? C(1) : A[j * LD + r]) * A[j * LD + i];
+                s0 = A[i * LD + i] * ((r == i) ? C(1) : A[i * LD + r]);   // j = i: T(i,i)=tau_i
+                int j = i + 1;
+                for (; j + 1 < r; j += 2) {
+                    s0 += A[j * LD + r] * A[j * LD + i];
+                    s1 += A[(j + 1) * LD + r] * A[(j + 1) * LD + i];
+                }
+                for (; j <= r; ++j) s0 += ((j == r) ? C(1) : A[j * LD + r]) * A[j * LD + i];
             }
-            Um[idx] = s;
+            Um[idx] = s0 + s1;
         }
+        __syncthreads();
+        mark(5);
     }
 
     // ---- tree: climb while we are the second arrival ----
@@ -326,6 +362,8 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
             }
             __syncthreads();
             if (s_old == 0) return;   // first arrival: the sibling continues
+            trc = g_panel_trace && b == 0 && parent < 64 ? g_panel_trace + (64 + j * 64 + parent) * 8 : nullptr;
+            mark(0);
             // combine: left leaf slot a = (2*parent) << (j-1), right b = (2*parent+1) << (j-1)
             const int64_t a = (parent << 1) << (j - 1);
             const int64_t bb = ((parent << 1) + 1) << (j - 1);
@@ -339,7 +377,9 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
                 }
             }
             __syncthreads();
-            tt_qr<C, TS>(Rt, Rb, tau, scal);
+            mark(1);
+            panel::tt_qr_la<C, TS, kNT>(Rt, Rb, tau, house);
+            mark(2);
             // R_top -> slot a
             C *Rg = ws.R + a * ts2;
             for (int idx = tid; idx < TS * TS; idx += kNT) {
@@ -350,16 +390,22 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
             for (int idx = tid; idx < TS * TS; idx += kNT) {
                 const int jj = idx / TS, i = idx % TS;
                 if (i < jj) {
-                    C s = C(0);
-                    for (int r = 0; r <= i; ++r) s += Rb[pk(r, i)] * Rb[pk(r, jj)];
-                    Tp[pk(i, jj)] = s;
+                    const C *vi = Rb + pk(0, i), *vj = Rb + pk(0, jj);
+                    C s0 = C(0), s1 = C(0);
+                    int r = 0;
+                    for (; r + 1 <= i; r += 2) {
+                        s0 += vi[r] * vj[r];
+                        s1 += vi[r + 1] * vj[r + 1];
+                    }
+                    if (r <= i) s0 += vi[r] * vj[r];
+                    Tp[pk(i, jj)] = s0 + s1;
                 }
             }
             __syncthreads();
-            build_T<C, TS>(tau, tmp,
-                           [&](int i, int jj) { return Tp[pk(i, jj)]; },
-                           [&](int i, int jj) { return Tp[pk(i, jj)]; },
-                           [&](int i, int jj, C v) { Tp[pk(i, jj)] = v; });
+            mark(3);
+            // Rt is saved: its space is the T-merge scratch
+            panel::build_T_rec<C, TS, kNT>(tau, Rt, [&](int i, int jj) -> C & { return Tp[pk(i, jj)]; });
+            mark(4);
             const int64_t slot = tree_offset(m, j) + parent;
             C *Vk = ws.Vk(slot), *Um = ws.Um(slot), *Tt = ws.Tt(slot);
             for (int idx = tid; idx < TS * TS; idx += kNT) {
@@ -373,6 +419,8 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
                 for (int jj = (i > r ? i : r); jj < TS; ++jj) s += Rb[pk(r, jj)] * Tp[pk(i, jj)];
                 Um[idx] = s;
             }
+            __syncthreads();
+            mark(5);
         }
         node = parent;
     }
@@ -655,6 +703,12 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
     };
     struct Mark { cudaEvent_t a, b, c; };
     std::vector<Mark> marks;
+    const char *trace_path = getenv("BSVD_PANEL_TRACE");
+    unsigned long long *trace_buf = nullptr;
+    if (trace_path) {
+        cudaMalloc(&trace_buf, 64 * 9 * 8 * 8);
+        cudaMemset(trace_buf, 0, 64 * 9 * 8 * 8);
+    }
     auto side = [&](int64_t k, bool lq) -> cudaError_t {
         View<S> V{a, lq ? n : 1, lq ? 1 : n};
         const int64_t top = lq ? k + 1 : k;
@@ -663,11 +717,22 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
         const int64_t ntrail = N - 1 - k;
         Mark mk{};
         if (timed) mk.a = ev();
+        const bool tr_this = trace_path && k == 4 && !lq;
+        if (tr_this) cudaMemcpyToSymbolAsync(g_panel_trace, &trace_buf, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
         k_panel_tree<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
             V, m, top, k, ws, ws_elems, a_bstride);
         bsvd_host::count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+        if (tr_this) {
+            void *null_ptr = nullptr;
+            cudaMemcpyToSymbolAsync(g_panel_trace, &null_ptr, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
+            std::vector<unsigned long long> h(64 * 9 * 8);
+            cudaMemcpyAsync(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            FILE *f = fopen(trace_path, "wb");
+            if (f) { fwrite(h.data(), 8, h.size(), f); fclose(f); }
+        }
         if (timed) mk.b = ev();
         if (ntrail > 0) {
             if constexpr (TS >= 16) {
