@@ -230,6 +230,7 @@ __device__ void tt_qr(C *Rt, C *Rb, C *tau, C *scal) {
 
 }  // namespace bsvd
 #include "panel_qr.cuh"
+#include "panel_blocked.cuh"
 namespace bsvd {
 
 // Development instrumentation (BSVD_PANEL_TRACE): leaf-phase timestamps of
@@ -428,6 +429,203 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
     __syncthreads();
     if (L == 0 || node == 0) {
         const C *Rg = ws.R;   // leaf slot 0
+        const int64_t r0 = top * TS, c0 = k * TS;
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            int r, c;
+            if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
+            if (r <= c) *V.ptr(r0 + r, c0 + c) = CV::st(__ldcg(Rg + c * TS + r));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Blocked panel kernel (ts >= 16): same tree and workspace contract as
+// k_panel_tree, node QRs by blk::qr_blocked (panel_blocked.cuh).  The TT
+// operand is held unpacked (2ts x ts) except for fp64 at ts = 128, which
+// would not fit shared memory and keeps the packed look-ahead TT-QR.
+template <typename C, int TS>
+struct PanelBlk {
+    static constexpr int NB = TS < 32 ? TS : 32;
+    static constexpr bool TT_BLOCKED = !(sizeof(C) == 8 && TS >= 128);
+    static constexpr int LDL = TS + 1;                        // leaf lda
+    static constexpr int LDT = 2 * TS + 1;                    // TT lda (unpacked)
+    static constexpr int AUX = 2 * NB * TS + NB * (NB + 1) + 8 * 34 + 8;
+    static constexpr int LEAF = TS * LDL + AUX;
+    static constexpr int PK = TS * (TS + 1) / 2;
+    static constexpr int TTN = TT_BLOCKED ? (TS * LDT + AUX) : (3 * PK);
+    static constexpr int UNION = LEAF > TTN ? LEAF : TTN;
+    static constexpr size_t smem = (size_t)(UNION + TS + 8) * sizeof(C);
+};
+
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t top, int64_t k,
+                                                  TreeWs<C> ws, int64_t ws_bstride,
+                                                  int64_t a_bstride) {
+    using CV = Conv<S, C>;
+    using PB = PanelBlk<C, TS>;
+    constexpr int NB = PB::NB;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *sm = (C *)smem_raw;
+    C *tau = sm + PB::UNION;
+    __shared__ int s_old;
+
+    const int64_t b = blockIdx.y;
+    V.base += b * a_bstride;
+    ws.nodes += b * ws_bstride;
+    ws.R += b * ws_bstride;
+    ws.cnt = (int *)((char *)ws.cnt + b * ws_bstride * (int64_t)sizeof(C));
+    const int64_t l = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS;
+    auto house = [](C a, C s, C &bb, C &t, C &sc) { house_scalars(a, s, bb, t, sc); };
+    unsigned long long *trc = g_panel_trace && b == 0 && l < 64 ? g_panel_trace + l * 8 : nullptr;
+    auto mark = [&](int ph) {
+        if (trc && tid == 0) trc[ph] = gtimer_ns();
+    };
+
+    // ---- leaf: blocked QR of view tile (top + l, k) ----
+    {
+        constexpr int lda = PB::LDL;
+        C *A = sm;
+        C *wbuf = A + TS * lda, *gbuf = wbuf + NB * TS, *tsub = gbuf + NB * TS, *red = tsub + NB * (NB + 1);
+        mark(0);
+        const int64_t r0 = (top + l) * TS, c0 = k * TS;
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            int r, c;
+            if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
+            A[c * lda + r] = CV::ld(*V.ptr(r0 + r, c0 + c));
+        }
+        __syncthreads();
+        mark(1);
+        C *Rg = ws.R + l * ts2;
+        // R column blocks are final right after their sub-panel: save them, then T
+        // may reuse the upper triangle (qr_blocked writes T block column j0 there).
+        blk::qr_blocked<C, TS, false, kNT>(A, lda, tau, A, lda, wbuf, tsub, gbuf, red, house,
+            [&](int j0) {
+                for (int idx = tid; idx < TS * NB; idx += kNT) {
+                    const int c = j0 + idx / TS, r = idx % TS;
+                    Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
+                }
+                __syncthreads();
+            }, (g_panel_trace && b == 0 && l == 0) ? g_panel_trace + 64 * 9 * 8 : nullptr);
+        mark(4);
+        // Vk[r][i] = V(r, i);  Um[i][r] = U(r, i) = sum_{j=i..r} V(r,j) T(i,j)
+        C *Vk = ws.Vk(l), *Um = ws.Um(l);
+        for (int idx = tid; idx < TS * TS; idx += kNT) {
+            const int r = idx / TS, i = idx % TS;
+            Vk[idx] = (r > i) ? A[i * lda + r] : (r == i ? C(1) : C(0));
+        }
+        blk::sgemm<C, 4, 4, kNT>(TS, TS, TS,
+            [&](int r, int j) { return r == j ? C(1) : (r > j ? A[j * lda + r] : C(0)); },   // V(r, j)
+            [&](int j, int i) { return j >= i ? A[j * lda + i] : C(0); },                   // T(i, j)
+            [&](int r, int i, C v) { Um[i * TS + r] = v; });
+        __syncthreads();
+        mark(5);
+    }
+
+    // ---- tree: climb while we are the second arrival ----
+    const int L = tree_levels(m);
+    int64_t node = l;
+    for (int j = 1; j <= L; ++j) {
+        const int64_t parent = node >> 1;
+        const bool has_right = ((parent << 1) + 1) < tree_count(m, j - 1);
+        if (has_right) {
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                int *cptr = ws.cnt + tree_offset(m, j) - m + parent;
+                s_old = atomicAdd(cptr, 1);
+                if (s_old == 1) *cptr = 0;   // self-cleaning for the next launch
+                __threadfence();
+            }
+            __syncthreads();
+            if (s_old == 0) return;
+            trc = g_panel_trace && b == 0 && parent < 64 ? g_panel_trace + (64 + j * 64 + parent) * 8 : nullptr;
+            mark(0);
+            const int64_t a = (parent << 1) << (j - 1);
+            const int64_t bb = ((parent << 1) + 1) << (j - 1);
+            const C *Ra_g = ws.R + a * ts2, *Rb_g = ws.R + bb * ts2;
+            C *Rg = ws.R + a * ts2;
+            const int64_t slot = tree_offset(m, j) + parent;
+            C *Vk = ws.Vk(slot), *Um = ws.Um(slot), *Tt = ws.Tt(slot);
+            if constexpr (PB::TT_BLOCKED) {
+                constexpr int lda = PB::LDT;
+                C *A = sm;
+                C *wbuf = A + TS * lda, *gbuf = wbuf + NB * TS, *tsub = gbuf + NB * TS, *red = tsub + NB * (NB + 1);
+                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                    const int c = idx / TS, r = idx % TS;
+                    A[c * lda + r] = (r <= c) ? __ldcg(Ra_g + idx) : C(0);
+                    A[c * lda + TS + r] = (r <= c) ? __ldcg(Rb_g + idx) : C(0);
+                }
+                __syncthreads();
+                mark(1);
+                blk::qr_blocked<C, TS, true, kNT>(A, lda, tau, A, lda, wbuf, tsub, gbuf, red, house,
+                    [&](int j0) {
+                        for (int idx = tid; idx < TS * NB; idx += kNT) {
+                            const int c = j0 + idx / TS, r = idx % TS;
+                            Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
+                        }
+                        __syncthreads();
+                    });
+                mark(4);
+                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                    const int r = idx / TS, i = idx % TS;   // Vk[r][i] = Vb(r,i); Tt[r][i] = T(r,i)
+                    Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
+                    Tt[idx] = (r <= i) ? A[i * lda + r] : C(0);
+                }
+                // U(r, i) = sum_{jj >= max(i, r)} Vb(r, jj) T(i, jj)
+                blk::sgemm<C, 4, 4, kNT>(TS, TS, TS,
+                    [&](int r, int jj) { return jj >= r ? A[jj * lda + TS + r] : C(0); },
+                    [&](int jj, int i) { return jj >= i ? A[jj * lda + i] : C(0); },
+                    [&](int r, int i, C v) { Um[i * TS + r] = v; });
+                __syncthreads();
+            } else {
+                constexpr int PK = PB::PK;
+                C *Rt = sm, *Rb = sm + PK, *Tp = sm + 2 * PK;
+                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                    const int c = idx / TS, r = idx % TS;
+                    if (r <= c) {
+                        Rt[pk(r, c)] = __ldcg(Ra_g + idx);
+                        Rb[pk(r, c)] = __ldcg(Rb_g + idx);
+                    }
+                }
+                __syncthreads();
+                mark(1);
+                panel::tt_qr_la<C, TS, kNT>(Rt, Rb, tau, house);
+                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                    const int c = idx / TS, r = idx % TS;
+                    Rg[idx] = (r <= c) ? Rt[pk(r, c)] : C(0);
+                }
+                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                    const int jj = idx / TS, i = idx % TS;
+                    if (i < jj) {
+                        const C *vi = Rb + pk(0, i), *vj = Rb + pk(0, jj);
+                        C s0 = C(0);
+                        for (int r = 0; r <= i; ++r) s0 += vi[r] * vj[r];
+                        Tp[pk(i, jj)] = s0;
+                    }
+                }
+                __syncthreads();
+                panel::build_T_rec<C, TS, kNT>(tau, Rt, [&](int i, int jj) -> C & { return Tp[pk(i, jj)]; });
+                mark(4);
+                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                    const int r = idx / TS, i = idx % TS;
+                    Vk[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
+                    Tt[idx] = (r <= i) ? Tp[pk(r, i)] : C(0);
+                }
+                blk::sgemm<C, 4, 4, kNT>(TS, TS, TS,
+                    [&](int r, int jj) { return jj >= r ? Rb[pk(r, jj)] : C(0); },
+                    [&](int jj, int i) { return jj >= i ? Tp[pk(i, jj)] : C(0); },
+                    [&](int r, int i, C v) { Um[i * TS + r] = v; });
+                __syncthreads();
+            }
+            mark(5);
+        }
+        node = parent;
+    }
+    __syncthreads();
+    if (L == 0 || node == 0) {
+        const C *Rg = ws.R;
         const int64_t r0 = top * TS, c0 = k * TS;
         for (int idx = tid; idx < TS * TS; idx += kNT) {
             int r, c;
@@ -674,12 +872,15 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
         if (err != cudaSuccess) return err;
     }
     const int depth = tree_levels(N) + 1;
-    const size_t psm = panel_smem<C, TS>();
+    const size_t psm = TS >= 16 ? PanelBlk<C, TS>::smem : panel_smem<C, TS>();
     const size_t tsm = trail_smem<C, TS>(depth);
     if (tsm > 220 * 1024 || psm > 220 * 1024) return cudaErrorInvalidConfiguration;
     static size_t psm_set = 0, tsm_set = 0;   // per instantiation
     if (psm > psm_set) {
-        err = cudaFuncSetAttribute(k_panel_tree<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+        if constexpr (TS >= 16)
+            err = cudaFuncSetAttribute(k_panel_blk<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+        else
+            err = cudaFuncSetAttribute(k_panel_tree<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
         if (err != cudaSuccess) return err;
         psm_set = psm;
     }
@@ -706,8 +907,8 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
     const char *trace_path = getenv("BSVD_PANEL_TRACE");
     unsigned long long *trace_buf = nullptr;
     if (trace_path) {
-        cudaMalloc(&trace_buf, 64 * 9 * 8 * 8);
-        cudaMemset(trace_buf, 0, 64 * 9 * 8 * 8);
+        cudaMalloc(&trace_buf, (64 * 9 * 8 + 256) * 8);
+        cudaMemset(trace_buf, 0, (64 * 9 * 8 + 256) * 8);
     }
     auto side = [&](int64_t k, bool lq) -> cudaError_t {
         View<S> V{a, lq ? n : 1, lq ? 1 : n};
@@ -719,15 +920,19 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
         if (timed) mk.a = ev();
         const bool tr_this = trace_path && k == 4 && !lq;
         if (tr_this) cudaMemcpyToSymbolAsync(g_panel_trace, &trace_buf, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
-        k_panel_tree<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
-            V, m, top, k, ws, ws_elems, a_bstride);
+        if constexpr (TS >= 16)
+            k_panel_blk<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
+                V, m, top, k, ws, ws_elems, a_bstride);
+        else
+            k_panel_tree<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
+                V, m, top, k, ws, ws_elems, a_bstride);
         bsvd_host::count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         if (tr_this) {
             void *null_ptr = nullptr;
             cudaMemcpyToSymbolAsync(g_panel_trace, &null_ptr, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
-            std::vector<unsigned long long> h(64 * 9 * 8);
+            std::vector<unsigned long long> h(64 * 9 * 8 + 256);
             cudaMemcpyAsync(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
             FILE *f = fopen(trace_path, "wb");
