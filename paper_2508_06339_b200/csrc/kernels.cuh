@@ -48,6 +48,10 @@ template <typename S, typename C, int TS>
 cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
                                 int64_t top, int64_t k, int64_t m, const C *nodes,
                                 int64_t ws_bstride, cudaStream_t st);
+template <typename S, typename C, int TS>
+cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
+                               int64_t top, int64_t k, int64_t m, const C *nodes,
+                               int64_t ws_bstride, int j, cudaStream_t st);
 
 // ---- stage2_chase.cu -------------------------------------------------------
 size_t chase_workspace_bytes(int64_t n, int bw, int64_t batch);

@@ -308,10 +308,58 @@ cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstrid
     return cudaSuccess;
 }
 
+// One tree level only (0 = the leaves, j >= 1 = the TT nodes of level j), for
+// the overlapped schedule where level j's update starts as soon as the panel
+// has produced level j's reflectors.
+template <typename S, typename C, int TS>
+cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
+                               int64_t top, int64_t k, int64_t m, const C *nodes,
+                               int64_t ws_bstride, int j, cudaStream_t st) {
+    using G = Geo<C, TS>;
+    const int64_t ncols = (n / TS - 1 - k) * TS;
+    if (ncols <= 0) return cudaSuccess;
+    View<S> V{a, lq ? n : 1, lq ? 1 : n};
+    const int64_t cbase = (k + 1) * TS;
+    const int64_t ts2x3 = 3 * (int64_t)TS * TS;
+    const unsigned gx = (unsigned)((ncols + G::BN - 1) / G::BN);
+    static size_t set_leaf = 0, set_tt = 0;
+    const size_t sl = apply_smem<C, TS>(false), stt = apply_smem<C, TS>(true);
+    cudaError_t e;
+    if (j == 0) {
+        if (sl > set_leaf) {
+            if ((e = cudaFuncSetAttribute(k_apply_leaf<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sl)) != cudaSuccess) return e;
+            set_leaf = sl;
+        }
+        k_apply_leaf<S, C, TS><<<dim3(gx, (unsigned)m, (unsigned)batch), apply::kNT, sl, st>>>(
+            V, top, cbase, ncols, nodes, ts2x3, ws_bstride, a_bstride);
+        bsvd_host::count_launch();
+        return cudaGetLastError();
+    }
+    if (stt > set_tt) {
+        if ((e = cudaFuncSetAttribute(k_apply_tt<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stt)) != cudaSuccess) return e;
+        set_tt = stt;
+    }
+    int64_t off = 0, cnt_prev = m;
+    for (int q = 1; q < j; ++q) {
+        off += cnt_prev;
+        cnt_prev = (m + ((int64_t)1 << q) - 1) >> q;
+    }
+    off += cnt_prev;                                     // tree_offset(m, j)
+    const int64_t pairs = cnt_prev / 2;
+    if (pairs <= 0) return cudaSuccess;
+    k_apply_tt<S, C, TS><<<dim3(gx, (unsigned)pairs, (unsigned)batch), apply::kNT, stt, st>>>(
+        V, top, cbase, ncols, nodes, ts2x3, off, j, ws_bstride, a_bstride);
+    bsvd_host::count_launch();
+    return cudaGetLastError();
+}
+
 #define INST(S, C, TS)                                                                         \
     template cudaError_t launch_apply_levels<S, C, TS>(S *, int64_t, int64_t, int64_t, bool,    \
                                                        int64_t, int64_t, int64_t, const C *,    \
-                                                       int64_t, cudaStream_t);
+                                                       int64_t, cudaStream_t);                  \
+    template cudaError_t launch_apply_level<S, C, TS>(S *, int64_t, int64_t, int64_t, bool,     \
+                                                      int64_t, int64_t, int64_t, const C *,     \
+                                                      int64_t, int, cudaStream_t);
 #define INST3(TS) INST(double, double, TS) INST(float, float, TS) INST(__half, float, TS)
 INST3(16)
 INST3(32)

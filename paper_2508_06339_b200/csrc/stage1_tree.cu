@@ -443,13 +443,15 @@ __global__ void __launch_bounds__(kNT) k_panel_tree(View<S> V, int64_t m, int64_
 // k_panel_tree, node QRs by blk::qr_blocked (panel_blocked.cuh).  The TT
 // operand is held unpacked (2ts x ts) except for fp64 at ts = 128, which
 // would not fit shared memory and keeps the packed look-ahead TT-QR.
+constexpr int kNTP = 512;         // blocked panel CTA: 16 warps hide the column-step latencies
+
 template <typename C, int TS>
 struct PanelBlk {
-    static constexpr int NB = TS < 32 ? TS : 32;
+    static constexpr int NB = blk::NBsel<C, TS>::v;
     static constexpr bool TT_BLOCKED = !(sizeof(C) == 8 && TS >= 128);
     static constexpr int LDL = TS + 1;                        // leaf lda
     static constexpr int LDT = 2 * TS + 1;                    // TT lda (unpacked)
-    static constexpr int AUX = 2 * NB * TS + NB * (NB + 1) + 8 * 34 + 8;
+    static constexpr int AUX = blk::aux_elems<C, TS>();
     static constexpr int LEAF = TS * LDL + AUX;
     static constexpr int PK = TS * (TS + 1) / 2;
     static constexpr int TTN = TT_BLOCKED ? (TS * LDT + AUX) : (3 * PK);
@@ -458,7 +460,7 @@ struct PanelBlk {
 };
 
 template <typename S, typename C, int TS>
-__global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t top, int64_t k,
+__global__ void __launch_bounds__(kNTP) k_panel_blk(View<S> V, int64_t m, int64_t top, int64_t k,
                                                   TreeWs<C> ws, int64_t ws_bstride,
                                                   int64_t a_bstride) {
     using CV = Conv<S, C>;
@@ -487,10 +489,10 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
     {
         constexpr int lda = PB::LDL;
         C *A = sm;
-        C *wbuf = A + TS * lda, *gbuf = wbuf + NB * TS, *tsub = gbuf + NB * TS, *red = tsub + NB * (NB + 1);
+        C *aux = A + TS * lda;
         mark(0);
         const int64_t r0 = (top + l) * TS, c0 = k * TS;
-        for (int idx = tid; idx < TS * TS; idx += kNT) {
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
             int r, c;
             if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
             A[c * lda + r] = CV::ld(*V.ptr(r0 + r, c0 + c));
@@ -500,9 +502,9 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
         C *Rg = ws.R + l * ts2;
         // R column blocks are final right after their sub-panel: save them, then T
         // may reuse the upper triangle (qr_blocked writes T block column j0 there).
-        blk::qr_blocked<C, TS, false, kNT>(A, lda, tau, A, lda, wbuf, tsub, gbuf, red, house,
+        blk::qr_blocked<C, TS, false, kNTP>(A, lda, tau, A, lda, aux, house,
             [&](int j0) {
-                for (int idx = tid; idx < TS * NB; idx += kNT) {
+                for (int idx = tid; idx < TS * NB; idx += kNTP) {
                     const int c = j0 + idx / TS, r = idx % TS;
                     Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
                 }
@@ -511,11 +513,11 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
         mark(4);
         // Vk[r][i] = V(r, i);  Um[i][r] = U(r, i) = sum_{j=i..r} V(r,j) T(i,j)
         C *Vk = ws.Vk(l), *Um = ws.Um(l);
-        for (int idx = tid; idx < TS * TS; idx += kNT) {
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
             const int r = idx / TS, i = idx % TS;
             Vk[idx] = (r > i) ? A[i * lda + r] : (r == i ? C(1) : C(0));
         }
-        blk::sgemm<C, 4, 4, kNT>(TS, TS, TS,
+        blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
             [&](int r, int j) { return r == j ? C(1) : (r > j ? A[j * lda + r] : C(0)); },   // V(r, j)
             [&](int j, int i) { return j >= i ? A[j * lda + i] : C(0); },                   // T(i, j)
             [&](int r, int i, C v) { Um[i * TS + r] = v; });
@@ -551,30 +553,30 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
             if constexpr (PB::TT_BLOCKED) {
                 constexpr int lda = PB::LDT;
                 C *A = sm;
-                C *wbuf = A + TS * lda, *gbuf = wbuf + NB * TS, *tsub = gbuf + NB * TS, *red = tsub + NB * (NB + 1);
-                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                C *aux = A + TS * lda;
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {
                     const int c = idx / TS, r = idx % TS;
                     A[c * lda + r] = (r <= c) ? __ldcg(Ra_g + idx) : C(0);
                     A[c * lda + TS + r] = (r <= c) ? __ldcg(Rb_g + idx) : C(0);
                 }
                 __syncthreads();
                 mark(1);
-                blk::qr_blocked<C, TS, true, kNT>(A, lda, tau, A, lda, wbuf, tsub, gbuf, red, house,
+                blk::qr_blocked<C, TS, true, kNTP>(A, lda, tau, A, lda, aux, house,
                     [&](int j0) {
-                        for (int idx = tid; idx < TS * NB; idx += kNT) {
+                        for (int idx = tid; idx < TS * NB; idx += kNTP) {
                             const int c = j0 + idx / TS, r = idx % TS;
                             Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
                         }
                         __syncthreads();
                     });
                 mark(4);
-                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {
                     const int r = idx / TS, i = idx % TS;   // Vk[r][i] = Vb(r,i); Tt[r][i] = T(r,i)
                     Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
                     Tt[idx] = (r <= i) ? A[i * lda + r] : C(0);
                 }
                 // U(r, i) = sum_{jj >= max(i, r)} Vb(r, jj) T(i, jj)
-                blk::sgemm<C, 4, 4, kNT>(TS, TS, TS,
+                blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
                     [&](int r, int jj) { return jj >= r ? A[jj * lda + TS + r] : C(0); },
                     [&](int jj, int i) { return jj >= i ? A[jj * lda + i] : C(0); },
                     [&](int r, int i, C v) { Um[i * TS + r] = v; });
@@ -582,7 +584,7 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
             } else {
                 constexpr int PK = PB::PK;
                 C *Rt = sm, *Rb = sm + PK, *Tp = sm + 2 * PK;
-                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {
                     const int c = idx / TS, r = idx % TS;
                     if (r <= c) {
                         Rt[pk(r, c)] = __ldcg(Ra_g + idx);
@@ -591,12 +593,12 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
                 }
                 __syncthreads();
                 mark(1);
-                panel::tt_qr_la<C, TS, kNT>(Rt, Rb, tau, house);
-                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                panel::tt_qr_la<C, TS, kNTP>(Rt, Rb, tau, house);
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {
                     const int c = idx / TS, r = idx % TS;
                     Rg[idx] = (r <= c) ? Rt[pk(r, c)] : C(0);
                 }
-                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {
                     const int jj = idx / TS, i = idx % TS;
                     if (i < jj) {
                         const C *vi = Rb + pk(0, i), *vj = Rb + pk(0, jj);
@@ -606,14 +608,14 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
                     }
                 }
                 __syncthreads();
-                panel::build_T_rec<C, TS, kNT>(tau, Rt, [&](int i, int jj) -> C & { return Tp[pk(i, jj)]; });
+                panel::build_T_rec<C, TS, kNTP>(tau, Rt, [&](int i, int jj) -> C & { return Tp[pk(i, jj)]; });
                 mark(4);
-                for (int idx = tid; idx < TS * TS; idx += kNT) {
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {
                     const int r = idx / TS, i = idx % TS;
                     Vk[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
                     Tt[idx] = (r <= i) ? Tp[pk(r, i)] : C(0);
                 }
-                blk::sgemm<C, 4, 4, kNT>(TS, TS, TS,
+                blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
                     [&](int r, int jj) { return jj >= r ? Rb[pk(r, jj)] : C(0); },
                     [&](int jj, int i) { return jj >= i ? Tp[pk(i, jj)] : C(0); },
                     [&](int r, int i, C v) { Um[i * TS + r] = v; });
@@ -627,12 +629,284 @@ __global__ void __launch_bounds__(kNT) k_panel_blk(View<S> V, int64_t m, int64_t
     if (L == 0 || node == 0) {
         const C *Rg = ws.R;
         const int64_t r0 = top * TS, c0 = k * TS;
-        for (int idx = tid; idx < TS * TS; idx += kNT) {
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
             int r, c;
             if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
             if (r <= c) *V.ptr(r0 + r, c0 + c) = CV::st(__ldcg(Rg + c * TS + r));
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Per-level panel kernels (ts >= 16).  Same node math as k_panel_blk, but one
+// launch per tree level, so the trailing update of level j (on a second
+// stream) can start as soon as level j's reflectors exist: the leaf-level
+// update -- the largest -- overlaps the whole TT climb.
+
+template <typename S, typename C, int TS>
+__device__ __forceinline__ void write_root_R(const View<S> &V, const C *Rg, int64_t top, int64_t k) {
+    using CV = Conv<S, C>;
+    const int64_t r0 = top * TS, c0 = k * TS;
+    for (int idx = threadIdx.x; idx < TS * TS; idx += blockDim.x) {
+        int r, c;
+        if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
+        if (r <= c) *V.ptr(r0 + r, c0 + c) = CV::st(__ldcg(Rg + c * TS + r));
+    }
+}
+
+// Leaves: grid (m, batch).
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(kNTP) k_panel_leaf(View<S> V, int64_t m, int64_t top, int64_t k,
+                                                    TreeWs<C> ws, int64_t ws_bstride,
+                                                    int64_t a_bstride) {
+    using CV = Conv<S, C>;
+    using PB = PanelBlk<C, TS>;
+    constexpr int NB = PB::NB;
+    constexpr int lda = PB::LDL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *sm = (C *)smem_raw;
+    C *tau = sm + PB::UNION;
+    const int64_t b = blockIdx.y, l = blockIdx.x;
+    V.base += b * a_bstride;
+    ws.nodes += b * ws_bstride;
+    ws.R += b * ws_bstride;
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS;
+    auto house = [](C a, C s, C &bb, C &t, C &sc) { house_scalars(a, s, bb, t, sc); };
+    C *A = sm, *aux = A + TS * lda;
+    const int64_t r0 = (top + l) * TS, c0 = k * TS;
+    for (int idx = tid; idx < TS * TS; idx += kNTP) {
+        int r, c;
+        if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % TS; r = idx / TS; }
+        A[c * lda + r] = CV::ld(*V.ptr(r0 + r, c0 + c));
+    }
+    __syncthreads();
+    C *Rg = ws.R + l * ts2;
+    blk::qr_blocked<C, TS, false, kNTP>(A, lda, tau, A, lda, aux, house, [&](int j0) {
+        for (int idx = tid; idx < TS * NB; idx += kNTP) {
+            const int c = j0 + idx / TS, r = idx % TS;
+            Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
+        }
+        __syncthreads();
+    });
+    C *Vk = ws.Vk(l), *Um = ws.Um(l);
+    for (int idx = tid; idx < TS * TS; idx += kNTP) {
+        const int r = idx / TS, i = idx % TS;
+        Vk[idx] = (r > i) ? A[i * lda + r] : (r == i ? C(1) : C(0));
+    }
+    blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+        [&](int r, int j) { return r == j ? C(1) : (r > j ? A[j * lda + r] : C(0)); },
+        [&](int j, int i) { return j >= i ? A[j * lda + i] : C(0); },
+        [&](int r, int i, C v) { Um[i * TS + r] = v; });
+    if (m == 1) {                         // the leaf is the root
+        __syncthreads();
+        write_root_R<S, C, TS>(V, Rg, top, k);
+    }
+}
+
+// TT nodes of level j: grid (pairs, batch); node p combines the R factors of
+// leaves a = (2p) << (j-1) and bb = (2p+1) << (j-1).
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(kNTP) k_panel_tt(View<S> V, int64_t m, int64_t top, int64_t k, int j,
+                                                  TreeWs<C> ws, int64_t ws_bstride,
+                                                  int64_t a_bstride) {
+    using PB = PanelBlk<C, TS>;
+    constexpr int NB = PB::NB;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *sm = (C *)smem_raw;
+    C *tau = sm + PB::UNION;
+    const int64_t b = blockIdx.y, parent = blockIdx.x;
+    V.base += b * a_bstride;
+    ws.nodes += b * ws_bstride;
+    ws.R += b * ws_bstride;
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS;
+    auto house = [](C a, C s, C &bb, C &t, C &sc) { house_scalars(a, s, bb, t, sc); };
+    const int64_t a = (parent << 1) << (j - 1);
+    const int64_t bb = ((parent << 1) + 1) << (j - 1);
+    const C *Ra_g = ws.R + a * ts2, *Rb_g = ws.R + bb * ts2;
+    C *Rg = ws.R + a * ts2;
+    const int64_t slot = tree_offset(m, j) + parent;
+    C *Vk = ws.Vk(slot), *Um = ws.Um(slot), *Tt = ws.Tt(slot);
+    if constexpr (PB::TT_BLOCKED) {
+        constexpr int lda = PB::LDT;
+        C *A = sm, *aux = A + TS * lda;
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int c = idx / TS, r = idx % TS;
+            A[c * lda + r] = (r <= c) ? __ldcg(Ra_g + idx) : C(0);
+            A[c * lda + TS + r] = (r <= c) ? __ldcg(Rb_g + idx) : C(0);
+        }
+        __syncthreads();
+        blk::qr_blocked<C, TS, true, kNTP>(A, lda, tau, A, lda, aux, house, [&](int j0) {
+            for (int idx = tid; idx < TS * NB; idx += kNTP) {
+                const int c = j0 + idx / TS, r = idx % TS;
+                Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
+            }
+            __syncthreads();
+        });
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int r = idx / TS, i = idx % TS;
+            Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
+            Tt[idx] = (r <= i) ? A[i * lda + r] : C(0);
+        }
+        blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+            [&](int r, int jj) { return jj >= r ? A[jj * lda + TS + r] : C(0); },
+            [&](int jj, int i) { return jj >= i ? A[jj * lda + i] : C(0); },
+            [&](int r, int i, C v) { Um[i * TS + r] = v; });
+    } else {
+        constexpr int PK = PB::PK;
+        C *Rt = sm, *Rb = sm + PK, *Tp = sm + 2 * PK;
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int c = idx / TS, r = idx % TS;
+            if (r <= c) {
+                Rt[pk(r, c)] = __ldcg(Ra_g + idx);
+                Rb[pk(r, c)] = __ldcg(Rb_g + idx);
+            }
+        }
+        __syncthreads();
+        panel::tt_qr_la<C, TS, kNTP>(Rt, Rb, tau, house);
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int c = idx / TS, r = idx % TS;
+            Rg[idx] = (r <= c) ? Rt[pk(r, c)] : C(0);
+        }
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int jj = idx / TS, i = idx % TS;
+            if (i < jj) {
+                const C *vi = Rb + pk(0, i), *vj = Rb + pk(0, jj);
+                C s0 = C(0);
+                for (int r = 0; r <= i; ++r) s0 += vi[r] * vj[r];
+                Tp[pk(i, jj)] = s0;
+            }
+        }
+        __syncthreads();
+        panel::build_T_rec<C, TS, kNTP>(tau, Rt, [&](int i, int jj) -> C & { return Tp[pk(i, jj)]; });
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int r = idx / TS, i = idx % TS;
+            Vk[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
+            Tt[idx] = (r <= i) ? Tp[pk(r, i)] : C(0);
+        }
+        blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+            [&](int r, int jj) { return jj >= r ? Rb[pk(r, jj)] : C(0); },
+            [&](int jj, int i) { return jj >= i ? Tp[pk(i, jj)] : C(0); },
+            [&](int r, int i, C v) { Um[i * TS + r] = v; });
+    }
+    if (gridDim.x == 1 && ((int64_t)1 << j) >= m) {   // the root level: R into the band tile
+        __syncthreads();
+        write_root_R<S, C, TS>(V, Rg, top, k);
+    }
+}
+
+// Overlapped stage 1: panel levels on `st`, trailing levels on a second
+// stream, one event per level; the next side's panel waits for the whole
+// trailing update (its panel is the top tile row/column of that update).
+template <typename S, typename C, int TS>
+static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride, void *wsp,
+                              cudaStream_t st, double *pms, double *tms, bool timed) {
+    using PB = PanelBlk<C, TS>;
+    const int64_t N = n / TS;
+    const int64_t ws_elems = (int64_t)tree_ws_elems<C>(N, TS);
+    const int64_t ts2 = (int64_t)TS * TS;
+    TreeWs<C> ws;
+    ws.nodes = (C *)wsp;
+    ws.R = ws.nodes + tree_slots(N) * 3 * ts2;
+    ws.cnt = (int *)(ws.R + N * ts2);
+    ws.ts2 = ts2;
+    cudaError_t err;
+    const size_t psm = PB::smem;
+    static size_t set = 0;
+    if (psm > set) {
+        if ((err = cudaFuncSetAttribute(k_panel_leaf<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
+        if ((err = cudaFuncSetAttribute(k_panel_tt<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
+        set = psm;
+    }
+    // second stream + events (per call; creation cost is microseconds)
+    cudaStream_t st2;
+    if ((err = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    const int Lmax = tree_levels(N);
+    std::vector<cudaEvent_t> lvl(Lmax + 1);
+    cudaEvent_t done;
+    for (auto &e : lvl) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    cudaEventRecord(done, st);                 // st2 starts after the work already queued on st
+    std::vector<cudaEvent_t> tev;             // timing: (p0, p1) on st, (t0, t1) on st2 per side
+    auto tmark = [&](cudaStream_t s) -> cudaEvent_t {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        tev.push_back(e);
+        return e;
+    };
+    struct Side { cudaEvent_t p0, p1, t0, t1; };
+    std::vector<Side> sides;
+    auto side = [&](int64_t k, bool lq) -> cudaError_t {
+        View<S> V{a, lq ? n : 1, lq ? 1 : n};
+        const int64_t top = lq ? k + 1 : k;
+        if (top >= N) return cudaSuccess;
+        const int64_t m = N - top;
+        const int L = tree_levels(m);
+        const bool trail = (N - 1 - k) > 0;
+        Side sd{};
+        cudaStreamWaitEvent(st, done, 0);
+        if (timed) sd.p0 = tmark(st);
+        k_panel_leaf<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, ws, ws_elems, a_bstride);
+        bsvd_host::count_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        cudaEventRecord(lvl[0], st);
+        if (trail) {
+            cudaStreamWaitEvent(st2, lvl[0], 0);
+            if (timed) sd.t0 = tmark(st2);
+            if ((e = launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, 0, st2)) != cudaSuccess) return e;
+        }
+        int64_t cnt_prev = m;
+        for (int j = 1; j <= L; ++j) {
+            const int64_t pairs = cnt_prev / 2;
+            if (pairs > 0) {
+                k_panel_tt<S, C, TS><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, j, ws, ws_elems, a_bstride);
+                bsvd_host::count_launch();
+                if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            }
+            cudaEventRecord(lvl[j], st);
+            if (trail && pairs > 0) {
+                cudaStreamWaitEvent(st2, lvl[j], 0);
+                if ((e = launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, j, st2)) != cudaSuccess) return e;
+            }
+            cnt_prev = (m + ((int64_t)1 << j) - 1) >> j;
+        }
+        if (timed) sd.p1 = tmark(st);
+        if (trail) {
+            if (timed) sd.t1 = tmark(st2);
+            cudaEventRecord(done, st2);
+        } else {
+            cudaEventRecord(done, st);
+        }
+        if (timed) sides.push_back(sd);
+        return cudaSuccess;
+    };
+    err = cudaSuccess;
+    for (int64_t k = 0; k < N - 1 && err == cudaSuccess; ++k) {
+        if ((err = side(k, false)) != cudaSuccess) break;
+        err = side(k, true);
+    }
+    if (err == cudaSuccess) err = side(N - 1, false);
+    cudaStreamWaitEvent(st, done, 0);          // stage 2 on `st` sees every update
+    if (timed) {
+        cudaStreamSynchronize(st);
+        for (const Side &sd : sides) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, sd.p0, sd.p1);
+            *pms += ms;
+            if (sd.t0) {
+                cudaEventElapsedTime(&ms, sd.t0, sd.t1);
+                *tms += ms;
+            }
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
+    for (auto &e : lvl) cudaEventDestroy(e);
+    cudaEventDestroy(done);
+    cudaStreamDestroy(st2);                    // deferred until its queued work completes
+    return err;
 }
 
 // ---------------------------------------------------------------------------
@@ -857,6 +1131,10 @@ template <typename S, typename C, int TS>
 static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, void *wsp,
                             cudaStream_t st, cudaEvent_t *ev_p, cudaEvent_t *ev_t, double *pms,
                             double *tms) {
+    if constexpr (TS >= 16) {
+        if (!getenv("BSVD_NO_OVERLAP"))
+            return run_levels<S, C, TS>(a, n, batch, a_bstride, wsp, st, pms, tms, ev_p != nullptr);
+    }
     const int64_t N = n / TS;
     const int64_t ws_elems = (int64_t)tree_ws_elems<C>(N, TS);
     const int64_t ts2 = (int64_t)TS * TS;
@@ -921,7 +1199,7 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
         const bool tr_this = trace_path && k == 4 && !lq;
         if (tr_this) cudaMemcpyToSymbolAsync(g_panel_trace, &trace_buf, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
         if constexpr (TS >= 16)
-            k_panel_blk<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
+            k_panel_blk<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(
                 V, m, top, k, ws, ws_elems, a_bstride);
         else
             k_panel_tree<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNT, psm, st>>>(
