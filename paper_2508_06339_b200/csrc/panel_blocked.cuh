@@ -70,77 +70,86 @@ __host__ __device__ constexpr int aux_elems() {
     return (TS + NB) * (NB + 1) + 2 * NB * TS + NB * (NB + 1) + 16 * 34 + 8;
 }
 
-// Step 1: register-resident factorisation of sub-panel J0.
+// Step 1: register-resident factorisation of sub-panel J0 by the first NWF
+// warps (named barrier 1); the remaining warps only join the final barrier.
+// Fewer, fatter warps: the per-step overheads that every warp pays (partial-
+// sum reductions, reflector scalars) shrink with the warp count, and only
+// the pivot lane forms v (broadcast by shuffle) -- the step is issue-bound.
 template <typename C, int TS, bool TT, int NB, int J0, int NT, typename HS>
 __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, HS house,
                                          unsigned long long *st) {
     constexpr int R = TT ? (2 * NB + J0) : (TS - J0);    // rows in the sub-panel's row list
-    constexpr int NW = NT / 32;
-    constexpr int RPW = R / NW;                          // exact: R is a multiple of 8
-    static_assert(R % NW == 0, "row list must split evenly over the warps");
+    constexpr int NWF = 8;   // measured: 8 warps beat 4 (latency) and 16 (issue)
+    constexpr int RPW = R / NWF;
+    static_assert(R % NWF == 0, "row list must split evenly over the factor warps");
+    static_assert(NT / 32 >= NWF, "not enough warps");
     const int warp = threadIdx.x >> 5, c = threadIdx.x & 31;
-    const int i0 = warp * RPW;
-    auto row = [](int i) { return TT ? (i < NB ? J0 + i : TS + (i - NB)) : (J0 + i); };
-    C x[RPW];
+    if (warp < NWF) {
+        const int i0 = warp * RPW;
+        auto row = [](int i) { return TT ? (i < NB ? J0 + i : TS + (i - NB)) : (J0 + i); };
+        auto fbar = []() { asm volatile("bar.sync 1, %0;" ::"n"(NWF * 32) : "memory"); };
+        C x[RPW];
 #pragma unroll
-    for (int q = 0; q < RPW; ++q) x[q] = (c < NB) ? A[(J0 + c) * lda + row(i0 + q)] : C(0);
-    C *sig_part = red, *alpha_s = red + NW, *dpart = red + NW + 2;
-    for (int kl = 0; kl < NB; ++kl) {
-        // row-list index i is on reflector kl (excluding its unit row kl)?
-        auto on_ref = [&](int i) { return TT ? (i >= NB && i - NB <= J0 + kl) : (i > kl); };
-        if (c == kl) {
-            C s0 = C(0), s1 = C(0);
+        for (int q = 0; q < RPW; ++q) x[q] = (c < NB) ? A[(J0 + c) * lda + row(i0 + q)] : C(0);
+        C *sig_part = red, *alpha_s = red + NWF, *dpart = red + NWF + 2;
+        for (int kl = 0; kl < NB; ++kl) {
+            // row-list index i is on reflector kl (excluding its unit row kl)?
+            auto on_ref = [&](int i) { return TT ? (i >= NB && i - NB <= J0 + kl) : (i > kl); };
+            if (c == kl) {
+                C s0 = C(0), s1 = C(0);
+#pragma unroll
+                for (int q = 0; q < RPW; ++q) {
+                    const int i = i0 + q;
+                    const C xv = on_ref(i) ? x[q] : C(0);
+                    if (q & 1) s1 += xv * xv; else s0 += xv * xv;
+                    if (i == kl) *alpha_s = x[q];
+                }
+                sig_part[warp] = s0 + s1;
+            }
+            fbar();
+            C sig = C(0);
+#pragma unroll
+            for (int w = 0; w < NWF; ++w) sig += sig_part[w];
+            C beta, t, scale;
+            house(*alpha_s, sig, beta, t, scale);
+            // the pivot lane forms v for this warp's rows; everyone gets it by shuffle
+            C v[RPW];
+            C d0 = C(0), d1 = C(0);
 #pragma unroll
             for (int q = 0; q < RPW; ++q) {
                 const int i = i0 + q;
-                const C xv = on_ref(i) ? x[q] : C(0);
-                if (q & 1) s1 += xv * xv; else s0 += xv * xv;
-                if (i == kl) *alpha_s = x[q];
+                const C mine = (i == kl) ? C(1) : (on_ref(i) ? x[q] * scale : C(0));
+                v[q] = __shfl_sync(0xffffffffu, mine, kl);
+                if (q & 1) d1 += v[q] * x[q]; else d0 += v[q] * x[q];
             }
-            sig_part[warp] = s0 + s1;
-        }
-        __syncthreads();
-        C sig = C(0);
+            dpart[warp * 32 + c] = d0 + d1;
+            fbar();
+            if (c > kl && c < NB) {
+                C dd = C(0);
 #pragma unroll
-        for (int w = 0; w < NW; ++w) sig += sig_part[w];
-        C beta, t, scale;
-        house(*alpha_s, sig, beta, t, scale);
-        C v[RPW];
-        C d0 = C(0), d1 = C(0);
+                for (int w = 0; w < NWF; ++w) dd += dpart[w * 32 + c];
+                const C wc = t * dd;
 #pragma unroll
-        for (int q = 0; q < RPW; ++q) {
-            const int i = i0 + q;
-            const C xk = __shfl_sync(0xffffffffu, x[q], kl);
-            v[q] = (i == kl) ? C(1) : (on_ref(i) ? xk * scale : C(0));
-            if (q & 1) d1 += v[q] * x[q]; else d0 += v[q] * x[q];
-        }
-        dpart[warp * 32 + c] = d0 + d1;
-        __syncthreads();
-        if (c > kl && c < NB) {
-            C dd = C(0);
+                for (int q = 0; q < RPW; ++q) x[q] -= wc * v[q];
+            } else if (c == kl) {
 #pragma unroll
-            for (int w = 0; w < NW; ++w) dd += dpart[w * 32 + c];
-            const C wc = t * dd;
-#pragma unroll
-            for (int q = 0; q < RPW; ++q) x[q] -= wc * v[q];
-        } else if (c == kl) {
-#pragma unroll
-            for (int q = 0; q < RPW; ++q) {
-                const int i = i0 + q;
-                x[q] = (i == kl) ? beta : (on_ref(i) ? v[q] : x[q]);
-                Vs[(i0 + q) * (NB + 1) + kl] = v[q];
+                for (int q = 0; q < RPW; ++q) {
+                    const int i = i0 + q;
+                    x[q] = (i == kl) ? beta : (on_ref(i) ? v[q] : x[q]);
+                    Vs[(i0 + q) * (NB + 1) + kl] = v[q];
+                }
+                if (warp == 0) tau[J0 + kl] = t;
             }
-            if (warp == 0) tau[J0 + kl] = t;
+            if (st && threadIdx.x == 0) {
+                unsigned long long tt;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+                st[J0 + kl] = tt;
+            }
         }
-        if (st && threadIdx.x == 0) {
-            unsigned long long tt;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-            st[J0 + kl] = tt;
-        }
+#pragma unroll
+        for (int q = 0; q < RPW; ++q)
+            if (c < NB) A[(J0 + c) * lda + row(i0 + q)] = x[q];
     }
-#pragma unroll
-    for (int q = 0; q < RPW; ++q)
-        if (c < NB) A[(J0 + c) * lda + row(i0 + q)] = x[q];
     __syncthreads();
 }
 

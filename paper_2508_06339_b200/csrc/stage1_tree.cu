@@ -820,14 +820,14 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         set = psm;
     }
     // second stream + events (per call; creation cost is microseconds)
-    cudaStream_t st2;
+    cudaStream_t caller = st, st2;
     if ((err = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking)) != cudaSuccess) return err;
     const int Lmax = tree_levels(N);
     std::vector<cudaEvent_t> lvl(Lmax + 1);
     cudaEvent_t done;
     for (auto &e : lvl) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-    cudaEventRecord(done, st);                 // st2 starts after the work already queued on st
+    cudaEventRecord(done, caller);             // both start after the caller's queued work
     std::vector<cudaEvent_t> tev;             // timing: (p0, p1) on st, (t0, t1) on st2 per side
     auto tmark = [&](cudaStream_t s) -> cudaEvent_t {
         cudaEvent_t e;
@@ -889,9 +889,11 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         err = side(k, true);
     }
     if (err == cudaSuccess) err = side(N - 1, false);
-    cudaStreamWaitEvent(st, done, 0);          // stage 2 on `st` sees every update
+    cudaEventRecord(lvl[0], st);
+    cudaStreamWaitEvent(caller, lvl[0], 0);    // stage 2 on the caller's stream sees
+    cudaStreamWaitEvent(caller, done, 0);      // every panel and trailing update
     if (timed) {
-        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(caller);
         for (const Side &sd : sides) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, sd.p0, sd.p1);

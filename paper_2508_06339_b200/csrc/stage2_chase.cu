@@ -87,16 +87,20 @@ __device__ __forceinline__ void cluster_sync() {
 // Householder generation (LAPACK dlarfg convention): x -> beta e1 with
 // H = I - tau v v^T, v[0] = 1.  Executed by warp 0 of every CTA of the
 // cluster (identical arithmetic -> identical v); v (len L) into vs.
-__device__ void make_reflector_warp(const Band &A, int64_t r0, int64_t c0, bool column, int L,
-                                    double *vs, double *tau_s, double *beta_s) {
+__device__ __forceinline__ void pivot_load(const Band &A, int64_t r0, int64_t c0, bool column, int L,
+                                           double (&x4)[4], double &alpha) {
     const int lane = threadIdx.x & 31;
-    const double alpha = __ldcg(A.at(r0, c0));
-    double x4[4];
+    alpha = __ldcg(A.at(r0, c0));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int j = 1 + lane + 32 * q;
         x4[q] = j < L ? (column ? __ldcg(A.at(r0 + j, c0)) : __ldcg(A.at(r0, c0 + j))) : 0.0;
     }
+}
+
+__device__ __forceinline__ void pivot_finish(const double (&x4)[4], double alpha, int L, double *vs,
+                                             double *tau_s, double *beta_s) {
+    const int lane = threadIdx.x & 31;
     double sig = 0.0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -130,19 +134,15 @@ __device__ void write_pivot(const Band &A, int64_t r0, int64_t c0, bool column, 
 
 // Left op slice: pivot column p (rows [p, p+L), L <= 128), this CTA's
 // columns [ca, cb) (<= 64).  Register tile: warp w owns columns w, w+8, ...;
-// lane l holds rows l, l+32, l+64, l+96 of each -- every load of the slice is
-// issued before the first use (one L2 round trip), no shared staging, no
-// per-element index division.
-__device__ void left_slice(const Band &A, int64_t p, int L, int64_t ca, int64_t cb,
-                           const double *vs, double tau) {
-    const int ncol = (int)(cb - ca);
-    if (ncol <= 0) return;
+// lane l holds rows l, l+32, l+64, l+96 of each.  The slice's loads are
+// issued BEFORE mid() (reflector formation + cluster barrier) so the two L2
+// round trips overlap; mid() must be reached by every thread.
+template <int CPW, typename Mid>
+__device__ __forceinline__ void left_slice(const Band &A, int64_t p, int L, int64_t ca, int64_t cb,
+                                           const double *vs, const double *tau_s, Mid mid) {
+    const int ncol = cb > ca ? (int)(cb - ca) : 0;      // <= 8 * CPW
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int CPW = 8;                      // columns per warp (64 / 8 warps)
     double x[CPW][4];
-    double v[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = (lane + 32 * q < L) ? vs[lane + 32 * q] : 0.0;
 #pragma unroll
     for (int k = 0; k < CPW; ++k) {
         const int c = warp + 8 * k;
@@ -153,6 +153,12 @@ __device__ void left_slice(const Band &A, int64_t p, int L, int64_t ca, int64_t 
             x[k][q] = (col && r < L) ? __ldcg(col + r) : 0.0;
         }
     }
+    mid();
+    const double tau = *tau_s;
+    if (tau == 0.0 || ncol == 0) return;
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = (lane + 32 * q < L) ? vs[lane + 32 * q] : 0.0;
     double w[CPW];
 #pragma unroll
     for (int k = 0; k < CPW; ++k) {
@@ -183,50 +189,58 @@ __device__ void left_slice(const Band &A, int64_t p, int L, int64_t ca, int64_t 
 // (coalesced column segments), warp w = (row half, column phase q of 4);
 // each thread holds columns q, q+4, ... of its row (<= 32 values); the four
 // column-phase partial dots are combined through shared memory.
-__device__ void right_slice(const Band &A, int64_t p, int64_t c0, int L, int64_t ra, int64_t rb,
-                            const double *vs, double tau, double *part) {
-    const int nrow = (int)(rb - ra);
-    if (nrow <= 0) return;
+template <int NH, typename Mid>
+__device__ __forceinline__ void right_slice(const Band &A, int64_t p, int64_t c0, int L, int64_t ra,
+                                            int64_t rb, const double *vs, const double *tau_s,
+                                            double *part, Mid mid) {
+    const int nrow = rb > ra ? (int)(rb - ra) : 0;      // <= 32 * NH
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int half = warp & 1, q = warp >> 1;           // 2 row halves x 4 column phases
+    constexpr int PH = 8 / NH;                          // column phases
+    const int half = warp % NH, q = warp / NH;
     const int r = half * 32 + lane;
     const bool act = r < nrow;
-    constexpr int JPT = 32;                             // columns per thread (128 / 4)
+    constexpr int JPT = 128 / PH;                       // columns per thread
     double x[JPT];
-    const double *base = A.at(ra + r, c0);              // column j at base + j*(ld-1)
     const int64_t cstride = A.ld - 1;                   // (r, c+1) - (r, c)
+    const double *base = act ? A.at(ra + r, c0) : nullptr;
 #pragma unroll
     for (int k = 0; k < JPT; ++k) {
-        const int j = q + 4 * k;
+        const int j = q + PH * k;
         x[k] = (act && j < L) ? __ldcg(base + (int64_t)j * cstride) : 0.0;
     }
+    mid();
+    const double tau = *tau_s;
+    if (tau == 0.0 || nrow == 0) return;                // uniform within the CTA
     double w = 0.0;
 #pragma unroll
     for (int k = 0; k < JPT; ++k) {
-        const int j = q + 4 * k;
+        const int j = q + PH * k;
         if (j < L) w += x[k] * vs[j];
     }
-    part[q * 64 + r] = w;
+    part[q * (32 * NH) + r] = w;
     __syncthreads();
-    const double tw = tau * (part[r] + part[64 + r] + part[128 + r] + part[192 + r]);
+    double ws = 0.0;
+#pragma unroll
+    for (int g = 0; g < PH; ++g) ws += part[g * (32 * NH) + r];
+    const double tw = tau * ws;
     if (act && ra + r != p) {
         double *rowp = A.at(ra + r, c0);
 #pragma unroll
         for (int k = 0; k < JPT; ++k) {
-            const int j = q + 4 * k;
+            const int j = q + PH * k;
             if (j < L) __stcg(rowp + (int64_t)j * cstride, x[k] - tw * vs[j]);
         }
     }
 }
 
-// One op (index i) of sweep s.  All CTAs of the cluster call this with the
-// same arguments; rank `rk` of CS owns a contiguous slice of the op.
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 
+// One op (index i) of sweep s.  All CTAs of the cluster call this with the
+// same arguments; rank `rk` of CS owns a contiguous slice of the op.
 template <int CS>
 __device__ void chase_op(const Band &A, int64_t s, int i, int64_t n, int b, unsigned rk,
                          double *vs, double *tau_s, double *beta_s, double *part,
@@ -252,21 +266,23 @@ __device__ void chase_op(const Band &A, int64_t s, int i, int64_t n, int b, unsi
         }
     }
     if (L < 2) return;                  // uniform across the cluster
-    if ((threadIdx.x >> 5) == 0)
-        make_reflector_warp(A, column ? p : p, c0, column, L, vs, tau_s, beta_s);
-    __syncthreads();
-    if (tr && threadIdx.x == 0) tr[2] = gtimer();
-    cluster_sync<CS>();                 // every CTA has read the pivot
-    if (tr && threadIdx.x == 0) tr[3] = gtimer();
-    const double tau = *tau_s;
-    if (rk == 0 && (threadIdx.x >> 5) == 0) write_pivot(A, p, c0, column, L, *beta_s);
-    if (tau != 0.0) {
-        const int64_t tot = hi - lo;
-        const int64_t chunk = (tot + CS - 1) / CS;
-        const int64_t a = lo + (int64_t)rk * chunk, e = min(a + chunk, hi);
-        if (column) left_slice(A, p, L, a, e, vs, tau);
-        else right_slice(A, p, c0, L, a, e, vs, tau, part);
-    }
+    const int64_t tot = hi - lo;
+    const int64_t chunk = (tot + CS - 1) / CS;
+    const int64_t a = lo + (int64_t)rk * chunk, e = min(a + chunk, hi);
+    double x4[4], alpha = 0.0;
+    if ((threadIdx.x >> 5) == 0) pivot_load(A, p, c0, column, L, x4, alpha);   // first in the LSU queue
+    auto mid = [&]() {
+        if ((threadIdx.x >> 5) == 0) pivot_finish(x4, alpha, L, vs, tau_s, beta_s);
+        __syncthreads();
+        if (tr && threadIdx.x == 0) tr[2] = gtimer();
+        cluster_sync<CS>();             // every CTA has read the pivot
+        if (tr && threadIdx.x == 0) tr[3] = gtimer();
+        if (rk == 0 && (threadIdx.x >> 5) == 0) write_pivot(A, p, c0, column, L, *beta_s);
+    };
+    constexpr int CPW = CS >= 8 ? 4 : 8;            // left slice <= 8*CPW columns
+    constexpr int NH = CS >= 8 ? 1 : 2;             // right slice <= 32*NH rows
+    if (column) left_slice<CPW>(A, p, L, a, e, vs, tau_s, mid);
+    else right_slice<NH>(A, p, c0, L, a, e, vs, tau_s, part, mid);
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[4] = gtimer();
     if (threadIdx.x == 0) __threadfence();   // publish this CTA's slice gpu-wide
@@ -294,7 +310,8 @@ __global__ void __launch_bounds__(256) k_chase(double *band, int64_t n, int b, i
             if (s > 0) {
                 if (threadIdx.x == 0) {
                     const int need = min(i + 4, nprev);
-                    while (ld_acquire(prog + s - 1) < need) __nanosleep(32);
+                    for (int spin = 0; ld_acquire(prog + s - 1) < need; ++spin)
+                        if (spin > 64) __nanosleep(20);
                     __threadfence();
                 }
                 __syncthreads();
@@ -371,7 +388,9 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         // matrices.  Shared slice: b x ceil(2b/CS) doubles.
         // Cluster size: every op is split over CS CTAs so each CTA's slice is
         // <= 64 columns (left op) or <= 64 rows (right op) of a register tile.
-        const int CS = b > 64 ? 4 : (b > 32 ? 2 : 1);
+        int CS = b > 64 ? 8 : (b > 32 ? 2 : 1);
+        if (const char *cs_env = getenv("BSVD_CHASE_CS")) CS = atoi(cs_env);
+        if (CS < 8 && b > 64) CS = 4;               // slices must fit the register tiles
         const size_t smem = 0;
         int64_t nitems = (n - 2) * batch;   // sweeps 0..n-3 do work (reference loop bound)
         // useful concurrency: a sweep trails its predecessor by 4 ops
@@ -389,7 +408,7 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         lc.attrs = attr;
         lc.numAttrs = 1;
         void (*kern)(double *, int64_t, int, int64_t, int64_t, int *, int64_t, unsigned long long *) =
-            CS == 4 ? k_chase<4> : (CS == 2 ? k_chase<2> : k_chase<1>);
+            CS == 8 ? k_chase<8> : (CS == 4 ? k_chase<4> : (CS == 2 ? k_chase<2> : k_chase<1>));
         if (CS > 1) {
             int max_clusters = 0;
             lc.gridDim = dim3((unsigned)(want * CS));
