@@ -80,7 +80,10 @@ __host__ __device__ inline int64_t tree_slots(int64_t N) { return 2 * N + 64; }
 template <typename C>
 __host__ __device__ inline size_t tree_ws_elems(int64_t N, int ts) {
     const int64_t ts2 = (int64_t)ts * ts;
-    return (size_t)(tree_slots(N) * 3 * ts2 + N * ts2) + (size_t)(N + 64) * sizeof(int) / sizeof(C) + 64;
+    // rounded to 64 elements: every batch member's slice stays 256-byte
+    // aligned for the 16-byte cp.async tile loads
+    const size_t e = (size_t)(tree_slots(N) * 3 * ts2 + N * ts2) + (size_t)(N + 64) * sizeof(int) / sizeof(C) + 64;
+    return (e + 63) & ~(size_t)63;
 }
 
 template <typename C>

@@ -137,15 +137,15 @@ __device__ void write_pivot(const Band &A, int64_t r0, int64_t c0, bool column, 
 // lane l holds rows l, l+32, l+64, l+96 of each.  The slice's loads are
 // issued BEFORE mid() (reflector formation + cluster barrier) so the two L2
 // round trips overlap; mid() must be reached by every thread.
-template <int CPW, typename Mid>
+template <int CPW, int NW, typename Mid>
 __device__ __forceinline__ void left_slice(const Band &A, int64_t p, int L, int64_t ca, int64_t cb,
                                            const double *vs, const double *tau_s, Mid mid) {
-    const int ncol = cb > ca ? (int)(cb - ca) : 0;      // <= 8 * CPW
+    const int ncol = cb > ca ? (int)(cb - ca) : 0;      // <= NW * CPW
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double x[CPW][4];
 #pragma unroll
     for (int k = 0; k < CPW; ++k) {
-        const int c = warp + 8 * k;
+        const int c = warp + NW * k;
         const double *col = (c < ncol) ? A.at(p, ca + c) : nullptr;   // rows contiguous
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -172,7 +172,7 @@ __device__ __forceinline__ void left_slice(const Band &A, int64_t p, int L, int6
         for (int k = 0; k < CPW; ++k) w[k] += __shfl_xor_sync(0xffffffffu, w[k], o);
 #pragma unroll
     for (int k = 0; k < CPW; ++k) {
-        const int c = warp + 8 * k;
+        const int c = warp + NW * k;
         if (c >= ncol) continue;
         double *col = A.at(p, ca + c);
         const double tw = tau * w[k];
@@ -189,13 +189,13 @@ __device__ __forceinline__ void left_slice(const Band &A, int64_t p, int L, int6
 // (coalesced column segments), warp w = (row half, column phase q of 4);
 // each thread holds columns q, q+4, ... of its row (<= 32 values); the four
 // column-phase partial dots are combined through shared memory.
-template <int NH, typename Mid>
+template <int NH, int NW, typename Mid>
 __device__ __forceinline__ void right_slice(const Band &A, int64_t p, int64_t c0, int L, int64_t ra,
                                             int64_t rb, const double *vs, const double *tau_s,
                                             double *part, Mid mid) {
     const int nrow = rb > ra ? (int)(rb - ra) : 0;      // <= 32 * NH
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int PH = 8 / NH;                          // column phases
+    constexpr int PH = NW / NH;                         // column phases
     const int half = warp % NH, q = warp / NH;
     const int r = half * 32 + lane;
     const bool act = r < nrow;
@@ -241,7 +241,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // One op (index i) of sweep s.  All CTAs of the cluster call this with the
 // same arguments; rank `rk` of CS owns a contiguous slice of the op.
-template <int CS>
+template <int CS, int NW = 8>
 __device__ void chase_op(const Band &A, int64_t s, int i, int64_t n, int b, unsigned rk,
                          double *vs, double *tau_s, double *beta_s, double *part,
                          unsigned long long *tr) {
@@ -279,10 +279,11 @@ __device__ void chase_op(const Band &A, int64_t s, int i, int64_t n, int b, unsi
         if (tr && threadIdx.x == 0) tr[3] = gtimer();
         if (rk == 0 && (threadIdx.x >> 5) == 0) write_pivot(A, p, c0, column, L, *beta_s);
     };
-    constexpr int CPW = CS >= 8 ? 4 : 8;            // left slice <= 8*CPW columns
-    constexpr int NH = CS >= 8 ? 1 : 2;             // right slice <= 32*NH rows
-    if (column) left_slice<CPW>(A, p, L, a, e, vs, tau_s, mid);
-    else right_slice<NH>(A, p, c0, L, a, e, vs, tau_s, part, mid);
+    // left slice <= NW*CPW columns, right slice <= 32*NH rows
+    constexpr int CPW = NW == 16 ? 8 : (CS >= 8 ? 4 : 8);
+    constexpr int NH = NW == 16 ? 4 : (CS >= 8 ? 1 : 2);
+    if (column) left_slice<CPW, NW>(A, p, L, a, e, vs, tau_s, mid);
+    else right_slice<NH, NW>(A, p, c0, L, a, e, vs, tau_s, part, mid);
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[4] = gtimer();
     if (threadIdx.x == 0) __threadfence();   // publish this CTA's slice gpu-wide
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(256) k_chase(double *band, int64_t n, int b, i
                                                int64_t batch, int *progress, int64_t nitems,
                                                unsigned long long *trace) {
     __shared__ double vs[128];
-    __shared__ double part[256];
+    __shared__ double part[512];
     __shared__ double tau_s, beta_s;
     const unsigned rk = CS > 1 ? cluster_rank() : 0;
     const int64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
@@ -321,6 +322,26 @@ __global__ void __launch_bounds__(256) k_chase(double *band, int64_t n, int b, i
             cluster_sync<CS>();         // all slices of op i are written
             if (rk == 0 && threadIdx.x == 0) st_release(prog + s, i + 1);
             if (tr && threadIdx.x == 0) tr[5] = gtimer();
+        }
+    }
+}
+
+// Batched chase for narrow bands (b <= 64): one 16-warp CTA owns whole
+// matrices and runs their sweeps back to back -- no inter-CTA progress
+// flags; with thousands of matrices the GPU is full without pipelining.
+__global__ void __launch_bounds__(512) k_chase_seq(double *band, int64_t n, int b, int64_t ld,
+                                                   int64_t batch) {
+    __shared__ double vs[128];
+    __shared__ double part[512];
+    __shared__ double tau_s, beta_s;
+    for (int64_t m = blockIdx.x; m < batch; m += gridDim.x) {
+        const Band A{band + m * n * ld, n, ld, b};
+        for (int64_t s = 0; s + 2 < n; ++s) {
+            const int nops = chase_nops(s, n, b);
+            for (int i = 0; i < nops; ++i) {
+                chase_op<1, 16>(A, s, i, n, b, 0, vs, &tau_s, &beta_s, part, nullptr);
+                __syncthreads();
+            }
         }
     }
 }
@@ -382,7 +403,16 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         bsvd_host::count_launch();
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
-    if (n > 2) {
+    if (n > 2 && b <= 64 && batch >= 512 && !getenv("BSVD_CHASE_PIPELINED")) {
+        int dev = 0, nsm = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chase_seq, 512, 0);
+        const int64_t grid = std::min<int64_t>(batch, (int64_t)nsm * std::max(per_sm, 1));
+        k_chase_seq<<<(unsigned)grid, 512, 0, st>>>(band, n, b, ld, batch);
+        bsvd_host::count_launch();
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    } else if (n > 2) {
         // Cluster size: a single large band splits every op over 4 CTAs (4x
         // the L2 bandwidth per op); batches get their parallelism from the
         // matrices.  Shared slice: b x ceil(2b/CS) doubles.

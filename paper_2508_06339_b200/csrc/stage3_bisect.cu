@@ -114,9 +114,7 @@ __device__ __forceinline__ void negcount2(const double *__restrict__ o2, int64_t
 // few ulps) the group finishes with plain bisection.  The invariant
 // N(lo) < rank <= N(hi) is the same, so the result is identical to bisection
 // to adjacent doubles.
-constexpr int kLanes = 8;
-
-template <typename OutT>
+template <int kLanes, typename OutT>
 __global__ void __launch_bounds__(128) k_bisect(const double *__restrict__ o2,
                                                 const double *__restrict__ scal, int64_t n,
                                                 int64_t n_out, OutT *__restrict__ out,
@@ -136,7 +134,7 @@ __global__ void __launch_bounds__(128) k_bisect(const double *__restrict__ o2,
         const double floor_ = 0x1p-120 * gersh;
         double lo = 0.0, hi = 2.0 * gersh;
         constexpr int NP = 2 * kLanes;                   // points per round
-        for (int round = 0; round < 40; ++round) {
+        for (int round = 0; round < (kLanes > 1 ? 40 : 0); ++round) {
             if (hi <= floor_) break;
             const double h = (hi - lo) / (NP + 1);
             const double x0 = lo + h * (2 * sub + 1), x1 = lo + h * (2 * sub + 2);
@@ -188,8 +186,15 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
     bsvd_host::count_launch();
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
-    dim3 grid((unsigned)((n_out * kLanes + 127) / 128), (unsigned)batch);
-    k_bisect<OutT><<<grid, 128, 0, st>>>(o2, scal, n, n_out, out, out_stride);
+    // Multisection when values are scarce (one large matrix), plain bisection
+    // (one lane per value, least total work) when a batch supplies the parallelism.
+    if (n_out * batch >= 131072) {
+        dim3 grid((unsigned)((n_out + 127) / 128), (unsigned)batch);
+        k_bisect<1, OutT><<<grid, 128, 0, st>>>(o2, scal, n, n_out, out, out_stride);
+    } else {
+        dim3 grid((unsigned)((n_out * 8 + 127) / 128), (unsigned)batch);
+        k_bisect<8, OutT><<<grid, 128, 0, st>>>(o2, scal, n, n_out, out, out_stride);
+    }
     bsvd_host::count_launch();
     return cudaGetLastError();
 }

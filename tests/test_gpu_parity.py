@@ -206,3 +206,19 @@ def test_timers(P, be_tree):
     P.svdvals(np.random.default_rng(0).standard_normal((256, 256)), backend=be_tree, timers=timers)
     assert set(timers) == set(P.PHASE_KEYS)
     assert all(v > 0 for v in timers.values())
+
+
+@pytest.mark.parametrize("n,ts", [(128, 64), (96, 32)])
+def test_large_batch_paths(P, be_tree, oracle, n, ts):
+    """Batches big enough for the one-CTA-per-matrix chase (batch >= 512,
+    b <= 64) and one-lane-per-value bisection (>= 131072 values)."""
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((1100, n, n)).astype(np.float32)
+    a[7] = 0.0                                   # an all-zero member
+    a[9] = np.diag(np.arange(n, 0, -1)).astype(np.float32)
+    got = P.svdvals_batched(a, P.KernelConfig(tilesize=ts), backend=be_tree)
+    assert got.shape == (1100, n)
+    assert not np.any(got[7])
+    assert np.array_equal(got[9], np.arange(n, 0, -1, dtype=np.float32))
+    for i in (0, 1, 550, 1099):
+        assert_close(got[i], oracle.svdvals(a[i].T.copy(), ts), np.float32, n, what=f"member {i}")
