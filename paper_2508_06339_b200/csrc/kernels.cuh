@@ -52,6 +52,11 @@ template <typename S, typename C, int TS>
 cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
                                int64_t top, int64_t k, int64_t m, const C *nodes,
                                int64_t ws_bstride, int j, cudaStream_t st);
+// Tensor-core (tcgen05 3xTF32) variant for fp32 compute at ts = 128.
+template <typename S>
+cudaError_t launch_apply_level_tc(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq, int64_t top,
+                                  int64_t k, int64_t m, const float *img, int64_t img_bstride, int j,
+                                  cudaStream_t st);
 
 // ---- stage2_chase.cu -------------------------------------------------------
 size_t chase_workspace_bytes(int64_t n, int bw, int64_t batch);

@@ -153,7 +153,7 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
     __syncthreads();
 }
 
-template <typename C, int TS, bool TT, int NB, int J0, int NT, typename HS, typename SaveR>
+template <typename C, int TS, bool TT, int NB, int J0, int NT, bool FULL_T, typename HS, typename SaveR>
 __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C *aux, HS house,
                                         SaveR save_r, unsigned long long *st) {
     if constexpr (J0 < TS) {
@@ -181,7 +181,9 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
         __syncthreads();
         panel::build_T_rec<C, NB, NT>(tau + J0, gbuf, [&](int i, int j) -> C & { return tsub[j * LDS + i]; });
         // ---- T[0:J0, J0:J0+NB] = -T[0:J0,0:J0] (Vprev^T Vs) T_sub
-        if constexpr (J0 > 0) {
+        // (FULL_T = false: only the diagonal blocks, which the factorisation
+        // itself needs; k_node_tu builds the rest off the critical path)
+        if constexpr (J0 > 0 && FULL_T) {
             // only rows where both can be nonzero: LEAF rows [J0,TS); TT bottom rows [0, J0+NB)
             constexpr int KLO = TT ? NB : 0;
             sgemm<C, 2, 2, NT>(J0, NB, R - KLO,
@@ -225,14 +227,14 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
             __syncthreads();
         }
         stamp(4 * (J0 / NB) + 2);
-        qr_step<C, TS, TT, NB, J0 + NB, NT>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
+        qr_step<C, TS, TT, NB, J0 + NB, NT, FULL_T>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
     }
 }
 
-template <typename C, int TS, bool TT, int NT, typename HS, typename SaveR>
+template <typename C, int TS, bool TT, int NT, bool FULL_T = true, typename HS, typename SaveR>
 __device__ void qr_blocked(C *A, int lda, C *tau, C *Tm, int ldt, C *aux, HS house, SaveR save_r,
                            unsigned long long *st = nullptr) {
-    qr_step<C, TS, TT, NBsel<C, TS>::v, 0, NT>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
+    qr_step<C, TS, TT, NBsel<C, TS>::v, 0, NT, FULL_T>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
 }
 
 }  // namespace blk

@@ -35,6 +35,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_sm100.cuh"
 
 namespace bsvd {
 
@@ -74,15 +75,32 @@ struct TreeWs {
     __host__ __device__ C *Tt(int64_t s) const { return nodes + s * 3 * ts2 + 2 * ts2; }
 };
 
-// sum_j ceil(m / 2^j) can exceed 2m (m = 5: 5+3+2+1 = 11): budget 2N + 64.
-__host__ __device__ inline int64_t tree_slots(int64_t N) { return 2 * N + 64; }
+// Exact slot count sum_j ceil(N / 2^j) down to the root (it can exceed 2N:
+// 5+3+2+1 = 11); the count is nondecreasing in m, so N bounds every side.
+__host__ __device__ inline int64_t tree_slots(int64_t N) {
+    int64_t s = 1;
+    for (int64_t c = N; c > 1; c = (c + 1) / 2) s += c;
+    return s + 8;
+}
+
+// Tensor-core trailing update (stage1_apply_tc.cu): fp32 compute, ts = 128.
+template <typename C>
+__host__ __device__ inline bool tree_tc(int ts) { return sizeof(C) == 4 && ts == 128; }
+
+// Elements before the tensor-core operand images (nodes | R | counters).
+template <typename C>
+__host__ __device__ inline size_t tree_img_offset(int64_t N, int ts) {
+    const int64_t ts2 = (int64_t)ts * ts;
+    const size_t e = (size_t)(tree_slots(N) * 3 * ts2 + N * ts2) + (size_t)(N + 64) * sizeof(int) / sizeof(C) + 64;
+    return (e + 63) & ~(size_t)63;
+}
 
 template <typename C>
 __host__ __device__ inline size_t tree_ws_elems(int64_t N, int ts) {
-    const int64_t ts2 = (int64_t)ts * ts;
     // rounded to 64 elements: every batch member's slice stays 256-byte
-    // aligned for the 16-byte cp.async tile loads
-    const size_t e = (size_t)(tree_slots(N) * 3 * ts2 + N * ts2) + (size_t)(N + 64) * sizeof(int) / sizeof(C) + 64;
+    // aligned for the 16-byte cp.async / bulk-copy tile loads
+    size_t e = tree_img_offset<C>(N, ts);
+    if (tree_tc<C>(ts)) e += (size_t)tree_slots(N) * 6 * ts * ts;   // hi/lo images, 3 per node
     return (e + 63) & ~(size_t)63;
 }
 
@@ -657,8 +675,91 @@ __device__ __forceinline__ void write_root_R(const View<S> &V, const C *Rg, int6
     }
 }
 
+// Deferred compact-WY factors.  The tree climb only needs each node's R, so
+// with DEFER the node kernels stop after the factorisation: they store V (Vk
+// slot) and tau (first TS entries of the Tt slot), and k_node_tu -- launched
+// on the trailing stream, off the panel's critical path -- builds T from
+// G = V^T V (build_T_rec) and U = V T^T for the level's trailing update.
+template <typename C, int TS>
+struct NodeTU {
+    static constexpr int LD = TS + 1;
+    static constexpr size_t smem = (size_t)(2 * TS * LD + TS * TS / 4 + TS) * sizeof(C);
+    static constexpr bool ok = smem <= 200 * 1024;
+};
+
+// With `img` (tensor-core trailing update, stage1_apply_tc.cu) the products
+// are written as pre-split, pre-swizzled K-major TF32 operand images instead
+// of Um / Tt: per node slot three A images of 2 ts^2 floats -- V^T (rows i,
+// K = r), then for a leaf U (rows r, K = i), for a TT node T^T and U -- each
+// K-block (32 of K) stored as [hi: ts rows x 32][lo: ts rows x 32].
+template <typename C, int TS>
+__device__ __forceinline__ void img_put(C *im, int m, int k, C v) {
+    if constexpr (sizeof(C) == 4) {
+        float h, l;
+        tc::split3(v, h, l);
+        const int o = (k >> 5) * (2 * TS * 32) + m * 32 + ((((k & 31) >> 2) ^ (m & 7)) << 2) + (k & 3);
+        im[o] = h;
+        im[o + TS * 32] = l;
+    }
+}
+
+template <typename C, int TS>
+__global__ void __launch_bounds__(kNTP) k_node_tu(C *nodes, int64_t slot0, int64_t ws_bstride,
+                                                 bool tt, C *img) {
+    using NT_ = NodeTU<C, TS>;
+    constexpr int LD = NT_::LD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *Vs = (C *)smem_raw;                 // Vs[i * LD + r] = V(r, i)
+    C *Ts = Vs + TS * LD;                  // Ts[j * LD + i] = T(i, j)
+    C *tmp = Ts + TS * LD;
+    C *tau = tmp + TS * TS / 4;
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS;
+    C *base = nodes + blockIdx.y * ws_bstride + (slot0 + blockIdx.x) * 3 * ts2;
+    C *Vk = base, *Um = base + ts2, *Tt = base + 2 * ts2;
+    C *im = img ? img + blockIdx.y * ws_bstride + (slot0 + blockIdx.x) * 6 * ts2 : nullptr;
+    for (int idx = tid; idx < TS * TS; idx += kNTP) {
+        const int r = idx / TS, i = idx % TS;
+        Vs[i * LD + r] = __ldcg(Vk + idx);
+    }
+    for (int i = tid; i < TS; i += kNTP) tau[i] = __ldcg(Tt + i);
+    __syncthreads();
+    // strictly upper G = V^T V (for TT nodes V = [I; Vb]: the identity adds only
+    // to the diagonal, so Vk = Vb gives the same G)
+    blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+        [&](int i, int r) { return Vs[i * LD + r]; },
+        [&](int r, int j) { return Vs[j * LD + r]; },
+        [&](int i, int j, C v) { if (i < j) Ts[j * LD + i] = v; });
+    __syncthreads();
+    panel::build_T_rec<C, TS, kNTP>(tau, tmp, [&](int i, int j) -> C & { return Ts[j * LD + i]; });
+    __syncthreads();
+    if (im) {
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int m = idx / TS, kk = idx % TS;
+            img_put<C, TS>(im, m, kk, Vs[m * LD + kk]);                        // V^T: (i, r) = V(r, i)
+            if (tt) img_put<C, TS>(im + 2 * ts2, m, kk, kk <= m ? Ts[m * LD + kk] : C(0));   // T^T: (r, i) = T(i, r)
+        }
+        C *imU = im + (tt ? 4 : 2) * ts2;
+        blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+            [&](int r, int j) { return Vs[j * LD + r]; },
+            [&](int j, int i) { return j >= i ? Ts[j * LD + i] : C(0); },
+            [&](int r, int i, C v) { img_put<C, TS>(imU, r, i, v); });
+        return;
+    }
+    if (tt)
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int r = idx / TS, i = idx % TS;   // Tt[r][i] = T(r, i)
+            Tt[idx] = (r <= i) ? Ts[i * LD + r] : C(0);
+        }
+    // U(r, i) = sum_{j >= i} V(r, j) T(i, j)
+    blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+        [&](int r, int j) { return Vs[j * LD + r]; },
+        [&](int j, int i) { return j >= i ? Ts[j * LD + i] : C(0); },
+        [&](int r, int i, C v) { Um[i * TS + r] = v; });
+}
+
 // Leaves: grid (m, batch).
-template <typename S, typename C, int TS>
+template <typename S, typename C, int TS, bool DEFER>
 __global__ void __launch_bounds__(kNTP) k_panel_leaf(View<S> V, int64_t m, int64_t top, int64_t k,
                                                     TreeWs<C> ws, int64_t ws_bstride,
                                                     int64_t a_bstride) {
@@ -685,7 +786,7 @@ __global__ void __launch_bounds__(kNTP) k_panel_leaf(View<S> V, int64_t m, int64
     }
     __syncthreads();
     C *Rg = ws.R + l * ts2;
-    blk::qr_blocked<C, TS, false, kNTP>(A, lda, tau, A, lda, aux, house, [&](int j0) {
+    blk::qr_blocked<C, TS, false, kNTP, !DEFER>(A, lda, tau, A, lda, aux, house, [&](int j0) {
         for (int idx = tid; idx < TS * NB; idx += kNTP) {
             const int c = j0 + idx / TS, r = idx % TS;
             Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
@@ -697,10 +798,14 @@ __global__ void __launch_bounds__(kNTP) k_panel_leaf(View<S> V, int64_t m, int64
         const int r = idx / TS, i = idx % TS;
         Vk[idx] = (r > i) ? A[i * lda + r] : (r == i ? C(1) : C(0));
     }
-    blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
-        [&](int r, int j) { return r == j ? C(1) : (r > j ? A[j * lda + r] : C(0)); },
-        [&](int j, int i) { return j >= i ? A[j * lda + i] : C(0); },
-        [&](int r, int i, C v) { Um[i * TS + r] = v; });
+    if constexpr (DEFER) {
+        for (int i = tid; i < TS; i += kNTP) ws.Tt(l)[i] = tau[i];
+    } else {
+        blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+            [&](int r, int j) { return r == j ? C(1) : (r > j ? A[j * lda + r] : C(0)); },
+            [&](int j, int i) { return j >= i ? A[j * lda + i] : C(0); },
+            [&](int r, int i, C v) { Um[i * TS + r] = v; });
+    }
     if (m == 1) {                         // the leaf is the root
         __syncthreads();
         write_root_R<S, C, TS>(V, Rg, top, k);
@@ -709,7 +814,7 @@ __global__ void __launch_bounds__(kNTP) k_panel_leaf(View<S> V, int64_t m, int64
 
 // TT nodes of level j: grid (pairs, batch); node p combines the R factors of
 // leaves a = (2p) << (j-1) and bb = (2p+1) << (j-1).
-template <typename S, typename C, int TS>
+template <typename S, typename C, int TS, bool DEFER>
 __global__ void __launch_bounds__(kNTP) k_panel_tt(View<S> V, int64_t m, int64_t top, int64_t k, int j,
                                                   TreeWs<C> ws, int64_t ws_bstride,
                                                   int64_t a_bstride) {
@@ -740,22 +845,30 @@ __global__ void __launch_bounds__(kNTP) k_panel_tt(View<S> V, int64_t m, int64_t
             A[c * lda + TS + r] = (r <= c) ? __ldcg(Rb_g + idx) : C(0);
         }
         __syncthreads();
-        blk::qr_blocked<C, TS, true, kNTP>(A, lda, tau, A, lda, aux, house, [&](int j0) {
+        blk::qr_blocked<C, TS, true, kNTP, !DEFER>(A, lda, tau, A, lda, aux, house, [&](int j0) {
             for (int idx = tid; idx < TS * NB; idx += kNTP) {
                 const int c = j0 + idx / TS, r = idx % TS;
                 Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
             }
             __syncthreads();
         });
-        for (int idx = tid; idx < TS * TS; idx += kNTP) {
-            const int r = idx / TS, i = idx % TS;
-            Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
-            Tt[idx] = (r <= i) ? A[i * lda + r] : C(0);
+        if constexpr (DEFER) {
+            for (int idx = tid; idx < TS * TS; idx += kNTP) {
+                const int r = idx / TS, i = idx % TS;
+                Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
+            }
+            for (int i = tid; i < TS; i += kNTP) Tt[i] = tau[i];
+        } else {
+            for (int idx = tid; idx < TS * TS; idx += kNTP) {
+                const int r = idx / TS, i = idx % TS;
+                Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
+                Tt[idx] = (r <= i) ? A[i * lda + r] : C(0);
+            }
+            blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
+                [&](int r, int jj) { return jj >= r ? A[jj * lda + TS + r] : C(0); },
+                [&](int jj, int i) { return jj >= i ? A[jj * lda + i] : C(0); },
+                [&](int r, int i, C v) { Um[i * TS + r] = v; });
         }
-        blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
-            [&](int r, int jj) { return jj >= r ? A[jj * lda + TS + r] : C(0); },
-            [&](int jj, int i) { return jj >= i ? A[jj * lda + i] : C(0); },
-            [&](int r, int i, C v) { Um[i * TS + r] = v; });
     } else {
         constexpr int PK = PB::PK;
         C *Rt = sm, *Rb = sm + PK, *Tp = sm + 2 * PK;
@@ -806,6 +919,7 @@ template <typename S, typename C, int TS>
 static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride, void *wsp,
                               cudaStream_t st, double *pms, double *tms, bool timed) {
     using PB = PanelBlk<C, TS>;
+    constexpr bool DEFER = NodeTU<C, TS>::ok;
     const int64_t N = n / TS;
     const int64_t ws_elems = (int64_t)tree_ws_elems<C>(N, TS);
     const int64_t ts2 = (int64_t)TS * TS;
@@ -816,15 +930,41 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     ws.ts2 = ts2;
     cudaError_t err;
     const size_t psm = PB::smem;
+    // tensor-core trailing update: fp32 compute at ts = 128 (BSVD_NO_TC=1 selects the FMA kernels)
+    C *img = ws.nodes + tree_img_offset<C>(N, TS);
+    const bool use_tc = DEFER && tree_tc<C>(TS) && !getenv("BSVD_NO_TC");
+    // T and U of `count` nodes from slot0 on, ahead of their trailing level (st2)
+    auto node_tu = [&](int64_t slot0, int64_t count, bool tt, cudaStream_t s2) -> cudaError_t {
+        if (!DEFER || count <= 0) return cudaSuccess;
+        k_node_tu<C, TS><<<dim3((unsigned)count, (unsigned)batch), kNTP, NodeTU<C, TS>::smem, s2>>>(
+            ws.nodes, slot0, ws_elems, tt, use_tc ? img : nullptr);
+        bsvd_host::count_launch();
+        return cudaGetLastError();
+    };
     static size_t set = 0;
     if (psm > set) {
-        if ((err = cudaFuncSetAttribute(k_panel_leaf<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
-        if ((err = cudaFuncSetAttribute(k_panel_tt<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
+        if ((err = cudaFuncSetAttribute(k_panel_leaf<S, C, TS, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
+        if ((err = cudaFuncSetAttribute(k_panel_tt<S, C, TS, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
+        if (DEFER && (err = cudaFuncSetAttribute(k_node_tu<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NodeTU<C, TS>::smem)) != cudaSuccess) return err;
         set = psm;
     }
     // second stream + events (per call; creation cost is microseconds)
-    cudaStream_t caller = st, st2;
+    cudaStream_t caller = st, st2, st1 = nullptr;
     if ((err = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    if (getenv("BSVD_PANEL_PRIO")) {          // experiment: panel levels on a high-priority stream
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if ((err = cudaStreamCreateWithPriority(&st1, cudaStreamNonBlocking, hi)) != cudaSuccess) return err;
+        st = st1;
+    }
+    auto apply_level = [&](bool lq, int64_t top, int64_t k, int64_t m, int j) -> cudaError_t {
+        if constexpr (sizeof(C) == 4 && TS == 128) {
+            if (use_tc)
+                return launch_apply_level_tc<S>(a, n, batch, a_bstride, lq, top, k, m, (const float *)img,
+                                                ws_elems, j, st2);
+        }
+        return launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, j, st2);
+    };
     const int Lmax = tree_levels(N);
     std::vector<cudaEvent_t> lvl(Lmax + 1);
     cudaEvent_t done;
@@ -851,7 +991,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         Side sd{};
         cudaStreamWaitEvent(st, done, 0);
         if (timed) sd.p0 = tmark(st);
-        k_panel_leaf<S, C, TS><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, ws, ws_elems, a_bstride);
+        k_panel_leaf<S, C, TS, DEFER><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, ws, ws_elems, a_bstride);
         bsvd_host::count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -859,20 +999,22 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if (trail) {
             cudaStreamWaitEvent(st2, lvl[0], 0);
             if (timed) sd.t0 = tmark(st2);
-            if ((e = launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, 0, st2)) != cudaSuccess) return e;
+            if ((e = node_tu(0, m, false, st2)) != cudaSuccess) return e;
+            if ((e = apply_level(lq, top, k, m, 0)) != cudaSuccess) return e;
         }
         int64_t cnt_prev = m;
         for (int j = 1; j <= L; ++j) {
             const int64_t pairs = cnt_prev / 2;
             if (pairs > 0) {
-                k_panel_tt<S, C, TS><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, j, ws, ws_elems, a_bstride);
+                k_panel_tt<S, C, TS, DEFER><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, j, ws, ws_elems, a_bstride);
                 bsvd_host::count_launch();
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
             cudaEventRecord(lvl[j], st);
             if (trail && pairs > 0) {
                 cudaStreamWaitEvent(st2, lvl[j], 0);
-                if ((e = launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, j, st2)) != cudaSuccess) return e;
+                if ((e = node_tu(tree_offset(m, j), pairs, true, st2)) != cudaSuccess) return e;
+                if ((e = apply_level(lq, top, k, m, j)) != cudaSuccess) return e;
             }
             cnt_prev = (m + ((int64_t)1 << j) - 1) >> j;
         }
@@ -911,6 +1053,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     for (auto &e : lvl) cudaEventDestroy(e);
     cudaEventDestroy(done);
     cudaStreamDestroy(st2);                    // deferred until its queued work completes
+    if (st1) cudaStreamDestroy(st1);
     return err;
 }
 
