@@ -26,6 +26,17 @@
 namespace bsvd {
 namespace blk {
 
+// phase stamps (development tracing): globaltimer, or SM clock for microbenchmarks
+__device__ __forceinline__ unsigned long long stamp_now() {
+#ifdef BSVD_STAMP_CLOCK
+    return (unsigned long long)clock64();
+#else
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+#endif
+}
+
 // Register-tiled product on shared-memory operands:
 //   out(m, n, sum_k a(m, k) * b(k, n))  for (m, n) in [0,M) x [0,N).
 template <typename C, int RM, int RN, int NT, typename AF, typename BF, typename OF>
@@ -67,7 +78,7 @@ struct NBsel {   // sub-panel width: 16 keeps fp64 ts=128 leaves inside shared m
 template <typename C, int TS>
 __host__ __device__ constexpr int aux_elems() {
     constexpr int NB = NBsel<C, TS>::v;
-    return (TS + NB) * (NB + 1) + 2 * NB * TS + NB * (NB + 1) + 16 * 34 + 8;
+    return (TS + NB) * (NB + 1) + 2 * NB * TS + NB * (NB + 1) + 16 * 34 + 8 + (TS + 2 * NB);
 }
 
 // Step 1: register-resident factorisation of sub-panel J0 by the first NWF
@@ -91,10 +102,19 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
         C x[RPW];
 #pragma unroll
         for (int q = 0; q < RPW; ++q) x[q] = (c < NB) ? A[(J0 + c) * lda + row(i0 + q)] : C(0);
+        // red: sig_part[NWF] | alpha | pad | dpart[NWF*32] | vbuf[R] (this warp's slab of v)
         C *sig_part = red, *alpha_s = red + NWF, *dpart = red + NWF + 2;
+        C *vbuf = dpart + NWF * 32 + i0;
         for (int kl = 0; kl < NB; ++kl) {
             // row-list index i is on reflector kl (excluding its unit row kl)?
             auto on_ref = [&](int i) { return TT ? (i >= NB && i - NB <= J0 + kl) : (i > kl); };
+#ifdef BSVD_QR_PROBE
+            const bool probe = st && J0 == 0 && kl == 5 && threadIdx.x == 64;
+#define PROBE(k) if (probe) st[200 + (k)] = stamp_now();
+#else
+#define PROBE(k)
+#endif
+            PROBE(0)
             if (c == kl) {
                 C s0 = C(0), s1 = C(0);
 #pragma unroll
@@ -107,23 +127,41 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
                 sig_part[warp] = s0 + s1;
             }
             fbar();
+            PROBE(1)
             C sig = C(0);
 #pragma unroll
             for (int w = 0; w < NWF; ++w) sig += sig_part[w];
             C beta, t, scale;
             house(*alpha_s, sig, beta, t, scale);
-            // the pivot lane forms v for this warp's rows; everyone gets it by shuffle
+            PROBE(2)
+            // the pivot lane forms v for this warp's rows (branch-free selects) and
+            // publishes it through shared memory; the warp reads it back broadcast
+            if (c == kl) {
+#pragma unroll
+                for (int q = 0; q < RPW; ++q) {
+                    const int i = i0 + q;
+                    C vq = x[q] * scale;
+                    vq = on_ref(i) ? vq : C(0);
+                    vq = (i == kl) ? C(1) : vq;
+                    vbuf[q] = vq;
+                    Vs[(i0 + q) * (NB + 1) + kl] = vq;
+                    x[q] = (i == kl) ? beta : (on_ref(i) ? vq : x[q]);
+                }
+                if (warp == 0) tau[J0 + kl] = t;
+            }
+            __syncwarp();
+            PROBE(3)
             C v[RPW];
             C d0 = C(0), d1 = C(0);
 #pragma unroll
             for (int q = 0; q < RPW; ++q) {
-                const int i = i0 + q;
-                const C mine = (i == kl) ? C(1) : (on_ref(i) ? x[q] * scale : C(0));
-                v[q] = __shfl_sync(0xffffffffu, mine, kl);
+                v[q] = vbuf[q];
                 if (q & 1) d1 += v[q] * x[q]; else d0 += v[q] * x[q];
             }
             dpart[warp * 32 + c] = d0 + d1;
+            PROBE(4)
             fbar();
+            PROBE(5)
             if (c > kl && c < NB) {
                 C dd = C(0);
 #pragma unroll
@@ -131,20 +169,10 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
                 const C wc = t * dd;
 #pragma unroll
                 for (int q = 0; q < RPW; ++q) x[q] -= wc * v[q];
-            } else if (c == kl) {
-#pragma unroll
-                for (int q = 0; q < RPW; ++q) {
-                    const int i = i0 + q;
-                    x[q] = (i == kl) ? beta : (on_ref(i) ? v[q] : x[q]);
-                    Vs[(i0 + q) * (NB + 1) + kl] = v[q];
-                }
-                if (warp == 0) tau[J0 + kl] = t;
             }
-            if (st && threadIdx.x == 0) {
-                unsigned long long tt;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-                st[J0 + kl] = tt;
-            }
+            PROBE(6)
+#undef PROBE
+            if (st && threadIdx.x == 0) st[J0 + kl] = stamp_now();
         }
 #pragma unroll
         for (int q = 0; q < RPW; ++q)
@@ -164,11 +192,7 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
         C *tsub = gbuf + NB * TS, *red = tsub + NB * LDS;
         auto row = [](int i) { return TT ? (i < NB ? J0 + i : TS + (i - NB)) : (J0 + i); };
         auto stamp = [&](int id) {
-            if (st && threadIdx.x == 0) {
-                unsigned long long tt;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-                st[128 + id] = tt;
-            }
+            if (st && threadIdx.x == 0) st[128 + id] = stamp_now();
         };
         subpanel<C, TS, TT, NB, J0, NT>(A, lda, tau, red, Vs, house, st);
         stamp(4 * (J0 / NB) + 0);

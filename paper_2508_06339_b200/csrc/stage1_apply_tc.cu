@@ -62,9 +62,18 @@ __device__ __forceinline__ void load_row16(const View<S> &V, int64_t r, int64_t 
                 const float4 f = __ldcg(reinterpret_cast<const float4 *>(p) + q);
                 v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
             }
-        } else {
+        } else {                                       // fp16 storage: two 16-byte loads
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = CV::ld(p[q]);
+            for (int q = 0; q < 2; ++q) {
+                const uint4 u = __ldcg(reinterpret_cast<const uint4 *>(p) + q);
+                const __half2 *h2 = reinterpret_cast<const __half2 *>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __half22float2(h2[e]);
+                    v[8 * q + 2 * e] = f.x;
+                    v[8 * q + 2 * e + 1] = f.y;
+                }
+            }
         }
     } else {                                           // column contiguous: coalesced over r
 #pragma unroll
@@ -82,7 +91,13 @@ __device__ __forceinline__ void store_row16(const View<S> &V, int64_t r, int64_t
                 reinterpret_cast<float4 *>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) p[q] = CV::st(v[q]);
+            for (int q = 0; q < 2; ++q) {
+                uint4 u;
+                __half2 *h2 = reinterpret_cast<__half2 *>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) h2[e] = __floats2half2_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+                reinterpret_cast<uint4 *>(p)[q] = u;
+            }
         }
     } else {
 #pragma unroll

@@ -137,6 +137,22 @@ __device__ __forceinline__ void house_scalars(C alpha, C sig, C &beta, C &tau, C
     }
 }
 
+// fp32: one correctly rounded sqrt and two correctly rounded reciprocals in
+// place of two IEEE divisions (shorter dependent chain in the panel's column
+// step; tau and scale stay within an ulp or two).
+__device__ __forceinline__ void house_scalars(float alpha, float sig, float &beta, float &tau, float &scale) {
+    if (sig == 0.f) {
+        beta = alpha;
+        tau = 0.f;
+        scale = 1.f;
+    } else {
+        beta = -copysignf(__fsqrt_rn(fmaf(alpha, alpha, sig)), alpha);
+        const float d = alpha - beta;
+        scale = __frcp_rn(d);
+        tau = -d * __frcp_rn(beta);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Leaf: Householder QR of one ts x ts tile held column-major in smem (ld =
 // ts+1), reference reflector scalars.  Afterwards: R in the upper triangle,
@@ -951,7 +967,8 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     // second stream + events (per call; creation cost is microseconds)
     cudaStream_t caller = st, st2, st1 = nullptr;
     if ((err = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking)) != cudaSuccess) return err;
-    if (getenv("BSVD_PANEL_PRIO")) {          // experiment: panel levels on a high-priority stream
+    if (!getenv("BSVD_PANEL_NOPRIO")) {       // panel levels on a high-priority stream: the
+                                              // critical path gets the next free SM slots
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         if ((err = cudaStreamCreateWithPriority(&st1, cudaStreamNonBlocking, hi)) != cudaSuccess) return err;
