@@ -67,6 +67,9 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed(int *p, int v) {   // after an explicit fence
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Cluster helpers (CS CTAs of one thread-block cluster cooperate on an op).
 __device__ __forceinline__ unsigned cluster_rank() {
@@ -378,9 +381,409 @@ __global__ void k_extract_bidiag(const double *__restrict__ band, int64_t n, int
     }
 }
 
+// ---------------------------------------------------------------------------
+// Chase v2 (64 < b <= 128): carried-block pipeline on a thread-block cluster.
+//
+// The footprint of every op is two b x b blocks, and consecutive ops of a
+// sweep share one of them:
+//   left op t  (r0 = s+1+t b):  D_t = [r0, r0+b) x [r0, r0+b)      (carried)
+//                               E_t = [r0, r0+b) x [r0+b, r0+2b)   (loaded)
+//   right op t:                 P_t = E_t                          (carried)
+//                               Q_t = [r0+b, r0+2b) x [r0+b, r0+2b) (loaded)
+//   and D_{t+1} = Q_t; op 0 (row s) loads Q_{-1} = [s+1, s+1+b)^2.
+// Block k of a sweep (the block op k loads) lives in the REGISTERS of CTA
+// k mod NC of the cluster for exactly two ops: op k (as the new block) and
+// op k+1 (as the carried block, whose first column / row is op k+1's pivot),
+// then it is stored.  Each op therefore needs one global block load (after
+// the inter-sweep dependency) and no global pivot round trip: the carrier
+// forms op k+1's pivot from its registers and ships the raw vector (1 KB)
+// to the next block's CTA through distributed shared memory, signalled on
+// an mbarrier; both CTAs form the identical reflector.  Dependency (checked
+// by exhaustive footprint enumeration, scripts/chase_dep_check.py): block k
+// of sweep s may be loaded once sweep s-1 has STORED blocks 0..k+2; stores
+// are published in block order with a release counter per sweep.
+namespace ch2 {
+constexpr int NW = 16, NTH = 512, BK = 128;
+
+__device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_remote(uint32_t a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t a) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void wait_local(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n\t}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+struct Blk {
+    int64_t R0, C0;
+    int nr, nc;
+};
+__device__ __forceinline__ Blk geom(int64_t s, int k, int64_t n, int b) {
+    Blk g;
+    if (k & 1) {
+        g.R0 = s + 1 + (int64_t)((k - 1) >> 1) * b;
+        g.C0 = g.R0 + b;
+    } else {
+        g.R0 = g.C0 = s + 1 + (int64_t)(k >> 1) * b;
+    }
+    g.nr = (int)max((int64_t)0, min((int64_t)b, n - g.R0));
+    g.nc = (int)max((int64_t)0, min((int64_t)b, n - g.C0));
+    return g;
+}
+
+// Householder scalars from the raw pivot vector p[0..L) (LAPACK dlarfg
+// convention, v = (1, p[1:] * scale)).  Every warp of every CTA computes them
+// from the same bytes in the same order (xor butterfly: identical in all
+// lanes), so the reflector is bit-identical everywhere.
+__device__ __forceinline__ void reflector(const double *p, int L, double &tau, double &scale,
+                                          double &beta) {
+    const int lane = threadIdx.x & 31;
+    double sg = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int j = lane + 32 * a;
+        const double t = (j >= 1 && j < L) ? p[j] : 0.0;
+        sg = fma(t, t, sg);
+    }
+    sg = warp_sum(sg);
+    const double alpha = p[0];
+    tau = 0.0;
+    scale = 0.0;
+    beta = alpha;
+    if (sg != 0.0) {
+        // norm = sqrt(alpha^2 + sg) via one reciprocal square root (two Newton
+        // steps on the hardware seed) instead of sqrt + two divisions:
+        // beta = -sign(alpha) norm, tau = 1 + |alpha|/norm,
+        // scale = 1/(alpha - beta) = sign(alpha)/(|alpha| + norm).
+        const double s2 = fma(alpha, alpha, sg);
+        double r = rsqrt(s2);
+        const double nrm = s2 * r;
+        const double aa = fabs(alpha);
+        beta = -copysign(nrm, alpha);
+        tau = fma(aa, r, 1.0);
+        scale = copysign(1.0 / (aa + nrm), alpha);
+    }
+}
+
+// Register tile: thread (warp w, lane l) holds rows l + 32a (a < 4) and
+// columns w + 16q (q < 8) of the 128 x 128 block -- one coalesced 256-byte
+// column segment per (a, q).
+__device__ __forceinline__ void load_blk(const Band &A, const Blk &g, double (&x)[4][8]) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int c = w + 16 * q;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = l + 32 * a;
+            x[a][q] = (r < g.nr && c < g.nc) ? __ldcg(A.at(g.R0 + r, g.C0 + c)) : 0.0;
+        }
+    }
+}
+// part: 0 all, 1 row 0 only, 2 column 0 only, 3 all but row 0, 4 all but column 0
+__device__ __forceinline__ void store_blk(const Band &A, const Blk &g, const double (&x)[4][8], int part) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int c = w + 16 * q;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = l + 32 * a;
+            const bool sel = part == 0 || (part == 1 && r == 0) || (part == 2 && c == 0) ||
+                             (part == 3 && r != 0) || (part == 4 && c != 0);
+            if (sel && r < g.nr && c < g.nc) __stcg(A.at(g.R0 + r, g.C0 + c), x[a][q]);
+        }
+    }
+}
+
+// Pivot hand-off for the next op: the emitting CTA writes the raw vector to
+// its own piv_self and to the receiving CTA's buffer (DSMEM).
+struct Emit {
+    double *self;      // nullptr: nothing to emit
+    uint32_t remote;   // cluster address of the receiver's buffer
+};
+__device__ __forceinline__ void emit_put(const Emit &e, int j, double v) {
+    e.self[j] = v;
+    st_remote(e.remote + 8u * (uint32_t)j, v);
+}
+
+// Sum of part[0..7] over the 32 lanes by recursive halving (9 shuffles, not
+// 40); every lane returns all eight totals (8 broadcast shuffles).  Lane l
+// owns total q = 4*bit4(l) + 2*bit3(l) + bit2(l) after the halving steps.
+__device__ __forceinline__ void lane_allreduce8(double (&part)[8]) {
+    const int l = threadIdx.x & 31;
+    double h4[4], h2[2], h1;
+    const bool b4 = l & 16, b3 = l & 8, b2 = l & 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double mine = b4 ? part[i + 4] : part[i], other = b4 ? part[i] : part[i + 4];
+        h4[i] = mine + __shfl_xor_sync(0xffffffffu, other, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double mine = b3 ? h4[i + 2] : h4[i], other = b3 ? h4[i] : h4[i + 2];
+        h2[i] = mine + __shfl_xor_sync(0xffffffffu, other, 8);
+    }
+    {
+        const double mine = b2 ? h2[1] : h2[0], other = b2 ? h2[0] : h2[1];
+        h1 = mine + __shfl_xor_sync(0xffffffffu, other, 4);
+    }
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) part[q] = __shfl_sync(0xffffffffu, h1, ((q >> 2) << 4) | (((q >> 1) & 1) << 3) | ((q & 1) << 2));
+}
+
+// Left reflector (rows of the block, pivot relative row 0) on every column:
+// column dots reduce over the lanes.  carrier: column 0 is the pivot column.
+// emit: row 0 after the update (the next right op's pivot) is shipped before
+// the rest of the block is updated.
+__device__ __forceinline__ void left_apply(double (&x)[4][8], const double *p, int L, double tau,
+                                           double scale, double beta, bool carrier, const Emit &em) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    double va[4], part[8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int j = l + 32 * a;
+        va[a] = j == 0 ? 1.0 : (j < L ? p[j] * scale : 0.0);
+    }
+    if (tau != 0.0) {                        // uniform across the CTA
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            double t = va[0] * x[0][q];
+#pragma unroll
+            for (int a = 1; a < 4; ++a) t = fma(va[a], x[a][q], t);
+            part[q] = t;
+        }
+        lane_allreduce8(part);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) part[q] *= tau;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) part[q] = 0.0;
+    }
+    if (em.self && l == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) emit_put(em, w + 16 * q, fma(-part[q], va[0], x[0][q]));
+    }
+    if (tau != 0.0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) x[a][q] = fma(-part[q], va[a], x[a][q]);
+    }
+    if (carrier && w == 0) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) x[a][0] = (l + 32 * a == 0) ? beta : 0.0;
+    }
+}
+
+// Right reflector (columns of the block, pivot relative column 0) on every
+// row: row dots reduce over the 16 warps through shared memory.
+// carrier: row 0 is the pivot row.  emit: column 0 after the update (the
+// next left op's pivot).
+__device__ __forceinline__ void right_apply(double (&x)[4][8], const double *p, int L, double tau,
+                                            double scale, double beta, bool carrier,
+                                            double (*red)[BK], double (*red2)[BK], const Emit &em) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, tid = threadIdx.x;
+    double vq[8], td[4];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int c = w + 16 * q;
+        vq[q] = c == 0 ? 1.0 : (c < L ? p[c] * scale : 0.0);
+    }
+    if (tau != 0.0) {                        // uniform across the CTA
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double t = x[a][0] * vq[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) t = fma(x[a][q], vq[q], t);
+            red[w][l + 32 * a] = t;
+        }
+        __syncthreads();
+        {
+            const int row = tid & (BK - 1), g = tid >> 7;
+            red2[g][row] = (red[4 * g][row] + red[4 * g + 1][row]) + (red[4 * g + 2][row] + red[4 * g + 3][row]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = l + 32 * a;
+            td[a] = tau * ((red2[0][r] + red2[1][r]) + (red2[2][r] + red2[3][r]));
+        }
+    } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) td[a] = 0.0;
+    }
+    if (em.self && w == 0) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) emit_put(em, l + 32 * a, fma(-td[a], vq[0], x[a][0]));
+    }
+    if (tau != 0.0) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x[a][q] = fma(-td[a], vq[q], x[a][q]);
+    }
+    if (carrier && l == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[0][q] = (w + 16 * q == 0) ? beta : 0.0;
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ int msg_index(const int (&mc)[NC], int k) {
+    const int dr = k % NC;
+    int base = 0;
+#pragma unroll
+    for (int r = 0; r < NC; ++r)
+        if (r == dr) base = mc[r];
+    return base + k / NC - (dr == 0 ? 1 : 0);
+}
+
+template <int NC>
+__global__ void __launch_bounds__(NTH, 1) k_chase2(double *band, int64_t n, int b, int64_t ld,
+                                                  int64_t batch, int *flags, int fstride,
+                                                  int64_t nitems, unsigned long long *trace) {
+    __shared__ double piv_self[BK];
+    __shared__ double piv0[BK];
+    __shared__ double piv_in[2][BK];
+    __shared__ double red[NW][BK];
+    __shared__ double red2[4][BK];
+    __shared__ __align__(8) uint64_t mbar[2];
+    const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+    const unsigned rank = cluster_rank();
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&mbar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&mbar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_sync<2>();
+    int mc[NC];
+#pragma unroll
+    for (int r = 0; r < NC; ++r) mc[r] = 0;
+    const int64_t cid = blockIdx.x / NC, ncl = gridDim.x / NC;
+    for (int64_t item = cid; item < nitems; item += ncl) {
+        const int64_t s = item / batch, m = item % batch;
+        const Band A{band + m * n * ld, n, ld, b};
+        int *fl = flags + (m * n + s) * (int64_t)fstride;     // fl[j]: block j stored
+        const int nops = chase_nops(s, n, b);
+        const int nprev = s > 0 ? chase_nops(s - 1, n, b) : 0;
+        for (int k = (int)rank; k < nops; k += NC) {
+            const Blk g = geom(s, k, n, b);
+            unsigned long long *tr =
+                (trace && m == 0 && s < 256 && k < 32 && tid == 0) ? trace + (s * 32 + k) * 8 : nullptr;
+            if (tr) tr[0] = gtimer();
+            if (s > 0) {
+                // sweep s-1 must have stored blocks 0..k (flag 2) and the
+                // edges of blocks k+1, k+2 (flag >= 1): the rows/columns of
+                // this block that lie in them (scripts/chase_dep_check.py);
+                // blocks below k-NC+1 were checked for this CTA's previous block
+                const int lo = k >= NC ? k - NC + 1 : 0;
+                const int j = lo + tid;
+                if (j < min(k + 3, nprev)) {
+                    const int want = j <= k ? 2 : 1;
+                    const int *f = fl - fstride + j;
+                    for (int spin = 0; ld_acquire(f) < want; ++spin)
+                        if (spin > 64) __nanosleep(32);
+                }
+                __syncthreads();
+            }
+            if (tr) tr[1] = gtimer();
+            double x[4][8];
+            load_blk(A, g, x);
+            const double *pv;
+            int L;
+            if (k == 0) {
+                L = (int)min((int64_t)b, n - s - 1);
+                for (int j = tid; j < BK; j += NTH) piv0[j] = j < L ? __ldcg(A.at(s, s + 1 + j)) : 0.0;
+                __syncthreads();
+                pv = piv0;
+            } else {
+                const int idx = msg_index<NC>(mc, k);
+                wait_local(saddr(&mbar[idx & 1]), (uint32_t)((idx >> 1) & 1));
+                if (tr) tr[2] = gtimer();
+                pv = piv_in[idx & 1];
+                const Blk gp = geom(s, k - 1, n, b);
+                L = (k & 1) ? gp.nr : gp.nc;
+            }
+            double tau, scale, beta;
+            reflector(pv, L, tau, scale, beta);
+            if (k == 0 && tid == 0) __stcg(A.at(s, s + 1), beta);
+            // op k on the new block; its update yields op k+1's pivot, which is
+            // shipped to the CTA holding block k+1 before the bulk update
+            Emit em{nullptr, 0u};
+            int idx1 = 0, dr = 0;
+            if (k + 1 < nops) {
+                dr = (k + 1) % NC;
+                idx1 = msg_index<NC>(mc, k + 1);
+                em.self = piv_self;
+                em.remote = mapa(saddr(&piv_in[idx1 & 1][0]), (uint32_t)dr);
+            }
+            if (k & 1) left_apply(x, pv, L, tau, scale, beta, false, em);
+            else right_apply(x, pv, L, tau, scale, beta, false, red, red2, em);
+            if (tr) tr[3] = gtimer();
+            if (k + 1 < nops) {
+                __syncthreads();                        // piv_self / remote writes done
+                if (tid == 0) arrive_remote(mapa(saddr(&mbar[idx1 & 1]), (uint32_t)dr));
+                if (tr) tr[4] = gtimer();
+                const int L1 = (k & 1) ? g.nc : g.nr;
+                reflector(piv_self, L1, tau, scale, beta);
+                const Emit none{nullptr, 0u};
+                if (k & 1) right_apply(x, piv_self, L1, tau, scale, beta, true, red, red2, none);
+                else left_apply(x, piv_self, L1, tau, scale, beta, true, none);
+            }
+            if (tr) tr[5] = gtimer();
+            // publish block k: its edge (row 0 of an even / Q-type block,
+            // column 0 of an odd / E-type block -- the part the next sweep's
+            // block k-2 / k-1 reads) first, then the rest
+            {
+                const bool row_edge = !(k & 1);
+                store_blk(A, g, x, row_edge ? 1 : 2);
+                __syncthreads();
+                if (tid == 0) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (tr) tr[6] = gtimer();
+                    st_relaxed(fl + k, 1);
+                }
+                store_blk(A, g, x, row_edge ? 3 : 4);
+                __syncthreads();
+                if (tid == 0) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    st_relaxed(fl + k, 2);
+                    if (tr) tr[7] = gtimer();
+                }
+            }
+        }
+        // messages each rank received in this sweep (blocks k >= 1, k = rank mod NC)
+#pragma unroll
+        for (int r = 0; r < NC; ++r) mc[r] += (r < nops ? (nops - r + NC - 1) / NC : 0) - (r == 0 ? 1 : 0);
+    }
+    cluster_sync<2>();
+}
+}  // namespace ch2
+
+// ops (= blocks) of sweep 0, the longest sweep: the per-sweep flag stride of
+// the carried-block chase
+static int chase_max_ops(int64_t n, int b) { return 3 + (int)(2 * ((n + b - 1) / b)); }
+
 size_t chase_workspace_bytes(int64_t n, int bw, int64_t batch) {
     const int64_t ld = 3 * (int64_t)bw + 1;
-    return (size_t)batch * (size_t)n * ((size_t)ld * sizeof(double) + sizeof(int)) + 512;
+    size_t flags = bw > 64 ? (size_t)batch * n * chase_max_ops(n, bw) * sizeof(int) : 0;
+    return (size_t)batch * (size_t)n * ((size_t)ld * sizeof(double) + sizeof(int)) + flags + 512;
 }
 
 template <typename S>
@@ -403,7 +806,58 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         bsvd_host::count_launch();
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
-    if (n > 2 && b <= 64 && batch >= 512 && !getenv("BSVD_CHASE_PIPELINED")) {
+    if (n > 2 && b > 64 && b <= ch2::BK && !getenv("BSVD_CHASE_V1")) {
+        // carried-block cluster pipeline (NC CTAs per sweep, 1 CTA per SM)
+        int NC = 3;
+        if (const char *e = getenv("BSVD_CHASE_NC")) NC = atoi(e);
+        if (NC < 2 || NC > 4) NC = 3;
+        const int64_t nitems = (n - 2) * batch;
+        const int64_t nops0 = 1 + 2 * ((n - 2 + b) / b);
+        int64_t want = std::min<int64_t>(nitems, batch * (nops0 / 4 + 2));
+        cudaLaunchConfig_t lc{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = NC;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        lc.blockDim = dim3(ch2::NTH);
+        lc.dynamicSmemBytes = 0;
+        lc.stream = st;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        void (*kern)(double *, int64_t, int, int64_t, int64_t, int *, int, int64_t, unsigned long long *) =
+            NC == 2 ? ch2::k_chase2<2> : (NC == 4 ? ch2::k_chase2<4> : ch2::k_chase2<3>);
+        int max_clusters = 0;
+        lc.gridDim = dim3((unsigned)(want * NC));
+        err = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &lc);
+        if (err != cudaSuccess) return err;
+        want = std::min<int64_t>(want, std::max(max_clusters, 1));
+        lc.gridDim = dim3((unsigned)(want * NC));
+        int64_t n_ = n, ld_ = ld, batch_ = batch;
+        int b_ = b;
+        const char *trace_path = getenv("BSVD_CHASE_TRACE");
+        unsigned long long *trace = nullptr;
+        const size_t trace_bytes = 256 * 32 * 8 * sizeof(unsigned long long);
+        if (trace_path) {
+            cudaMallocAsync((void **)&trace, trace_bytes, st);
+            cudaMemsetAsync(trace, 0, trace_bytes, st);
+        }
+        int *flags = progress + batch * n;
+        const int fstride = chase_max_ops(n, b);
+        err = cudaMemsetAsync(flags, 0, (size_t)batch * n * fstride * sizeof(int), st);
+        if (err != cudaSuccess) return err;
+        err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, flags, fstride, nitems, trace);
+        bsvd_host::count_launch();
+        if (err != cudaSuccess) return err;
+        if (trace) {
+            std::vector<unsigned long long> h(trace_bytes / 8);
+            cudaMemcpyAsync(h.data(), trace, trace_bytes, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            FILE *f = fopen(trace_path, "wb");
+            if (f) { fwrite(h.data(), 1, trace_bytes, f); fclose(f); }
+            cudaFreeAsync(trace, st);
+        }
+    } else if (n > 2 && b <= 64 && batch >= 512 && !getenv("BSVD_CHASE_PIPELINED")) {
         int dev = 0, nsm = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -222,3 +222,27 @@ def test_large_batch_paths(P, be_tree, oracle, n, ts):
     assert np.array_equal(got[9], np.arange(n, 0, -1, dtype=np.float32))
     for i in (0, 1, 550, 1099):
         assert_close(got[i], oracle.svdvals(a[i].T.copy(), ts), np.float32, n, what=f"member {i}")
+
+
+@pytest.mark.parametrize("n", [3, 5, 127, 128, 129, 200, 256, 257, 300, 385, 640])
+def test_chase_wide_band(P, be_tree, oracle, n):
+    """Band width 128 runs the carried-block cluster chase (stage2_chase.cu
+    ch2): ragged tails (n not a multiple of b), blocks clipped to one row or
+    column, and sweeps shorter than the cluster."""
+    rng = np.random.default_rng(n)
+    a = np.triu(rng.standard_normal((n, n)))
+    a -= np.triu(a, 129)
+    d, e = P.band_to_bidiagonal(a, 128, backend=be_tree)
+    got = oracle.bidiagonal_values(d, e)
+    want = np.linalg.svd(a, compute_uv=False)
+    assert_close(got, want, np.float64, n, what=f"chase b=128 n={n}")
+
+
+def test_chase_wide_band_batched(P, be_tree, oracle):
+    rng = np.random.default_rng(77)
+    a = rng.standard_normal((5, 300, 300)).astype(np.float32)
+    a[2] = np.diag(np.arange(300, 0, -1)).astype(np.float32)
+    got = P.svdvals_batched(a, P.KernelConfig(tilesize=128), backend=be_tree)
+    assert np.array_equal(got[2], np.arange(300, 0, -1, dtype=np.float32))
+    for i in (0, 1, 3, 4):
+        assert_close(got[i], oracle.svdvals(a[i].T.copy(), 128), np.float32, 300, what=f"member {i}")
