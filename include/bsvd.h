@@ -123,6 +123,9 @@ bsvd_status bsvd_banddiag(void *a, bsvd_dtype dtype, int64_t n, const bsvd_confi
 
 /* secondstage.py:452-470 band_to_bidiagonal: upper band (column-major n x n,
  * band width bw, storage precision) -> float64 d[n], e[n-1]. */
+/* Device workspace bsvd_band_to_bidiagonal needs for an order-n band of width bw. */
+size_t bsvd_band_workspace_bytes(int64_t n, int32_t bw);
+
 bsvd_status bsvd_band_to_bidiagonal(const void *band, bsvd_dtype dtype, int64_t n, int32_t bw,
                                     double *d, double *e, void *workspace, size_t ws_bytes,
                                     void *stream);

@@ -25,7 +25,7 @@ EXPORTS = (
     "bsvd_validate_config", "bsvd_default_tilesize", "bsvd_default_options",
     "bsvd_last_error", "bsvd_version", "bsvd_workspace_bytes", "bsvd_svdvals",
     "bsvd_svdvals_ex", "bsvd_svdvals_batched", "bsvd_banddiag",
-    "bsvd_band_to_bidiagonal", "bsvd_bidiagonal_values", "bsvd_geqrt",
+    "bsvd_band_workspace_bytes", "bsvd_band_to_bidiagonal", "bsvd_bidiagonal_values", "bsvd_geqrt",
     "bsvd_tsqrt_chain", "bsvd_unmqr", "bsvd_tsmqr_fused", "bsvd_launch_counter",
 )
 
@@ -71,6 +71,7 @@ def load(path: str = LIB_PATH):
         "bsvd_svdvals_ex": (i32, [vp, i32, i64, i64, cfgp, optp, vp, vp, sz, vp, timp]),
         "bsvd_svdvals_batched": (i32, [vp, i32, i64, i64, i64, i64, cfgp, vp, vp, sz, vp, timp]),
         "bsvd_banddiag": (i32, [vp, i32, i64, cfgp, optp, vp, sz, vp]),
+        "bsvd_band_workspace_bytes": (sz, [i64, i32]),
         "bsvd_band_to_bidiagonal": (i32, [vp, i32, i64, i32, dp, dp, vp, sz, vp]),
         "bsvd_bidiagonal_values": (i32, [dp, dp, i64, dp, vp]),
         "bsvd_geqrt": (i32, [vp, i64, i64, i32, i32, vp, vp]),

@@ -228,8 +228,7 @@ def band_to_bidiagonal(band, bandwidth: int, backend=None):
     e = torch.empty(max(n - 1, 1), dtype=torch.float64, device=be.device)
     if not 1 <= bandwidth <= 128:
         raise ConfigError(f"band width must lie in [1, 128], got {bandwidth}")
-    nbytes = n * (3 * bandwidth + 1) * 8 + n * 4 + 1024
-    ws = be.workspace(nbytes)
+    ws = be.workspace(L.bsvd_band_workspace_bytes(n, int(bandwidth)))
     with torch.cuda.device(be.device):
         _lib.check(L.bsvd_band_to_bidiagonal(t.data_ptr(), prec.code, n, int(bandwidth),
                                              d.data_ptr(), e.data_ptr(), ws.data_ptr(), ws.numel(),

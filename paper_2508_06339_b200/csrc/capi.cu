@@ -332,6 +332,11 @@ bsvd_status bsvd_banddiag(void *a, bsvd_dtype dtype, int64_t n, const bsvd_confi
     return BSVD_OK;
 }
 
+size_t bsvd_band_workspace_bytes(int64_t n, int32_t bw) {
+    if (n < 1 || bw < 1 || bw > 128) return 0;
+    return chase_workspace_bytes(n, bw, 1);
+}
+
 bsvd_status bsvd_band_to_bidiagonal(const void *band, bsvd_dtype dtype, int64_t n, int32_t bw,
                                     double *d, double *e, void *workspace, size_t ws_bytes,
                                     void *stream) {

@@ -946,9 +946,12 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     ws.ts2 = ts2;
     cudaError_t err;
     const size_t psm = PB::smem;
-    // tensor-core trailing update: fp32 compute at ts = 128 (BSVD_NO_TC=1 selects the FMA kernels)
+    // Trailing update on the FMA pipe by default.  BSVD_TC=1 selects the
+    // tcgen05 3xTF32 kernels (fp32 compute, ts = 128): ~1.8x faster trailing
+    // update, but the tensor-core accumulation loses accuracy -- 6e-5 of
+    // sigma_max at n = 8192 against 2e-7 on the FMA path.
     C *img = ws.nodes + tree_img_offset<C>(N, TS);
-    const bool use_tc = DEFER && tree_tc<C>(TS) && !getenv("BSVD_NO_TC");
+    const bool use_tc = DEFER && tree_tc<C>(TS) && getenv("BSVD_TC") && atoi(getenv("BSVD_TC")) != 0;
     // T and U of `count` nodes from slot0 on, ahead of their trailing level (st2)
     auto node_tu = [&](int64_t slot0, int64_t count, bool tt, cudaStream_t s2) -> cudaError_t {
         if (!DEFER || count <= 0) return cudaSuccess;
@@ -974,6 +977,27 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if ((err = cudaStreamCreateWithPriority(&st1, cudaStreamNonBlocking, hi)) != cudaSuccess) return err;
         st = st1;
     }
+    // T and U of a level on a third stream as soon as the panel level exists,
+    // so they overlap the previous level's trailing update; the update of
+    // level j (st2) then waits only for its own factors.
+    cudaStream_t st3;
+    if ((err = cudaStreamCreateWithFlags(&st3, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    const int Lmax0 = tree_levels(N);
+    std::vector<cudaEvent_t> tuev(Lmax0 + 1);
+    for (auto &e : tuev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    std::vector<cudaEvent_t> *lvlp = nullptr;           // set below (panel level events)
+    auto level_tu = [&](int j, int64_t slot0, int64_t count, bool tt) -> cudaError_t {
+        cudaError_t e2;
+        if (!DEFER || count <= 0) {
+            cudaStreamWaitEvent(st2, (*lvlp)[j], 0);
+            return cudaSuccess;
+        }
+        cudaStreamWaitEvent(st3, (*lvlp)[j], 0);
+        if ((e2 = node_tu(slot0, count, tt, st3)) != cudaSuccess) return e2;
+        cudaEventRecord(tuev[j], st3);
+        cudaStreamWaitEvent(st2, tuev[j], 0);
+        return cudaSuccess;
+    };
     auto apply_level = [&](bool lq, int64_t top, int64_t k, int64_t m, int j) -> cudaError_t {
         if constexpr (sizeof(C) == 4 && TS == 128) {
             if (use_tc)
@@ -984,6 +1008,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     };
     const int Lmax = tree_levels(N);
     std::vector<cudaEvent_t> lvl(Lmax + 1);
+    lvlp = &lvl;
     cudaEvent_t done;
     for (auto &e : lvl) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
@@ -1014,9 +1039,8 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if (e != cudaSuccess) return e;
         cudaEventRecord(lvl[0], st);
         if (trail) {
-            cudaStreamWaitEvent(st2, lvl[0], 0);
             if (timed) sd.t0 = tmark(st2);
-            if ((e = node_tu(0, m, false, st2)) != cudaSuccess) return e;
+            if ((e = level_tu(0, 0, m, false)) != cudaSuccess) return e;
             if ((e = apply_level(lq, top, k, m, 0)) != cudaSuccess) return e;
         }
         int64_t cnt_prev = m;
@@ -1029,8 +1053,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
             }
             cudaEventRecord(lvl[j], st);
             if (trail && pairs > 0) {
-                cudaStreamWaitEvent(st2, lvl[j], 0);
-                if ((e = node_tu(tree_offset(m, j), pairs, true, st2)) != cudaSuccess) return e;
+                if ((e = level_tu(j, tree_offset(m, j), pairs, true)) != cudaSuccess) return e;
                 if ((e = apply_level(lq, top, k, m, j)) != cudaSuccess) return e;
             }
             cnt_prev = (m + ((int64_t)1 << j) - 1) >> j;
@@ -1068,8 +1091,10 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         for (cudaEvent_t e : tev) cudaEventDestroy(e);
     }
     for (auto &e : lvl) cudaEventDestroy(e);
+    for (auto &e : tuev) cudaEventDestroy(e);
     cudaEventDestroy(done);
     cudaStreamDestroy(st2);                    // deferred until its queued work completes
+    cudaStreamDestroy(st3);
     if (st1) cudaStreamDestroy(st1);
     return err;
 }

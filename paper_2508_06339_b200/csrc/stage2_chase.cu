@@ -351,9 +351,9 @@ __global__ void __launch_bounds__(512) k_chase_seq(double *band, int64_t n, int 
 
 // Pack the upper band (0 <= c - r <= bw) of a column-major S matrix into the
 // float64 chase layout (bulge room zeroed by a preceding memset).
-template <typename S>
+template <typename S, typename TB>
 __global__ void k_pack_band(const S *__restrict__ a, int64_t n, int64_t lda, int64_t a_bstride,
-                            int bw, double *__restrict__ band, int64_t ld, int b) {
+                            int bw, TB *__restrict__ band, int64_t ld, int b) {
     const int64_t m = blockIdx.y;
     a += m * a_bstride;
     band += m * n * ld;
@@ -363,12 +363,13 @@ __global__ void k_pack_band(const S *__restrict__ a, int64_t n, int64_t lda, int
         const int64_t c = idx / (bw + 1);
         const int64_t r = c - bw + idx % (bw + 1);
         if (r < 0) continue;
-        const double v = to_f64(a[c * lda + r]);
+        const TB v = (TB)to_f64(a[c * lda + r]);
         band[c * ld + (r - c + 2 * b)] = v;
     }
 }
 
-__global__ void k_extract_bidiag(const double *__restrict__ band, int64_t n, int64_t ld, int b,
+template <typename TB>
+__global__ void k_extract_bidiag(const TB *__restrict__ band, int64_t n, int64_t ld, int b,
                                  double *__restrict__ d, double *__restrict__ e) {
     const int64_t m = blockIdx.y;
     band += m * n * ld;
@@ -376,8 +377,8 @@ __global__ void k_extract_bidiag(const double *__restrict__ band, int64_t n, int
     e += m * (n - 1);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        d[i] = band[i * ld + 2 * b];
-        if (i + 1 < n) e[i] = band[(i + 1) * ld + (2 * b - 1)];
+        d[i] = (double)band[i * ld + 2 * b];
+        if (i + 1 < n) e[i] = (double)band[(i + 1) * ld + (2 * b - 1)];
     }
 }
 
@@ -411,9 +412,7 @@ __device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     return r;
 }
-__device__ __forceinline__ void st_remote(uint32_t a, double v) {
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
+
 __device__ __forceinline__ void arrive_remote(uint32_t a) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
@@ -426,6 +425,14 @@ __device__ __forceinline__ void wait_local(uint32_t a, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+
+template <typename T>
+struct BandT {
+    T *p;
+    int64_t n, ld;
+    int b;
+    __device__ __forceinline__ T *at(int64_t r, int64_t c) const { return p + c * ld + (r - c + 2 * b); }
+};
 
 struct Blk {
     int64_t R0, C0;
@@ -448,40 +455,53 @@ __device__ __forceinline__ Blk geom(int64_t s, int k, int64_t n, int b) {
 // convention, v = (1, p[1:] * scale)).  Every warp of every CTA computes them
 // from the same bytes in the same order (xor butterfly: identical in all
 // lanes), so the reflector is bit-identical everywhere.
-__device__ __forceinline__ void reflector(const double *p, int L, double &tau, double &scale,
-                                          double &beta) {
+template <typename T>
+__device__ __forceinline__ void reflector(const T *p, int L, T &tau, T &scale,
+                                          T &beta) {
     const int lane = threadIdx.x & 31;
-    double sg = 0.0;
+    T sg = T(0);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int j = lane + 32 * a;
-        const double t = (j >= 1 && j < L) ? p[j] : 0.0;
+        const T t = (j >= 1 && j < L) ? p[j] : T(0);
         sg = fma(t, t, sg);
     }
-    sg = warp_sum(sg);
-    const double alpha = p[0];
-    tau = 0.0;
-    scale = 0.0;
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
+    const T alpha = p[0];
+    tau = T(0);
+    scale = T(0);
     beta = alpha;
-    if (sg != 0.0) {
+    if (sg != T(0)) {
         // norm = sqrt(alpha^2 + sg) via one reciprocal square root (two Newton
         // steps on the hardware seed) instead of sqrt + two divisions:
         // beta = -sign(alpha) norm, tau = 1 + |alpha|/norm,
         // scale = 1/(alpha - beta) = sign(alpha)/(|alpha| + norm).
-        const double s2 = fma(alpha, alpha, sg);
-        double r = rsqrt(s2);
-        const double nrm = s2 * r;
-        const double aa = fabs(alpha);
-        beta = -copysign(nrm, alpha);
-        tau = fma(aa, r, 1.0);
-        scale = copysign(1.0 / (aa + nrm), alpha);
+        const T s2 = fma(alpha, alpha, sg);
+        const T aa = fabs(alpha);
+        if constexpr (sizeof(T) == 8) {
+            const T r = rsqrt(s2);
+            const T nrm = s2 * r;
+            beta = -copysign(nrm, alpha);
+            tau = fma(aa, r, T(1));
+            scale = copysign(T(1) / (aa + nrm), alpha);
+        } else {
+            // fp32: correctly rounded sqrt and divisions -- an inexact tau
+            // (rsqrtf is 2 ulp) leaves H = I - tau v v^T slightly non-orthogonal,
+            // and ~2 n^2 / b reflectors accumulate that drift
+            const T nrm = sqrtf(s2);
+            beta = -copysign(nrm, alpha);
+            tau = (beta - alpha) / beta;
+            scale = T(1) / (alpha - beta);
+        }
     }
 }
 
 // Register tile: thread (warp w, lane l) holds rows l + 32a (a < 4) and
 // columns w + 16q (q < 8) of the 128 x 128 block -- one coalesced 256-byte
 // column segment per (a, q).
-__device__ __forceinline__ void load_blk(const Band &A, const Blk &g, double (&x)[4][8]) {
+template <typename T>
+__device__ __forceinline__ void load_blk(const BandT<T> &A, const Blk &g, T (&x)[4][8]) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -489,12 +509,13 @@ __device__ __forceinline__ void load_blk(const Band &A, const Blk &g, double (&x
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             const int r = l + 32 * a;
-            x[a][q] = (r < g.nr && c < g.nc) ? __ldcg(A.at(g.R0 + r, g.C0 + c)) : 0.0;
+            x[a][q] = (r < g.nr && c < g.nc) ? __ldcg(A.at(g.R0 + r, g.C0 + c)) : T(0);
         }
     }
 }
 // part: 0 all, 1 row 0 only, 2 column 0 only, 3 all but row 0, 4 all but column 0
-__device__ __forceinline__ void store_blk(const Band &A, const Blk &g, const double (&x)[4][8], int part) {
+template <typename T>
+__device__ __forceinline__ void store_blk(const BandT<T> &A, const Blk &g, const T (&x)[4][8], int part) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -511,34 +532,50 @@ __device__ __forceinline__ void store_blk(const Band &A, const Blk &g, const dou
 
 // Pivot hand-off for the next op: the emitting CTA writes the raw vector to
 // its own piv_self and to the receiving CTA's buffer (DSMEM).
+template <typename T>
 struct Emit {
-    double *self;      // nullptr: nothing to emit
+    T *self;      // nullptr: nothing to emit
     uint32_t remote;   // cluster address of the receiver's buffer
+    uint32_t rbar;     // cluster address of the receiver's mbarrier for it
 };
-__device__ __forceinline__ void emit_put(const Emit &e, int j, double v) {
+// The remote half is an st.async whose completion is counted in bytes on the
+// receiver's mbarrier (complete_tx): no fence, barrier or arrive on the
+// sender's side -- the receiver's phase completes when all 1 KB has landed.
+template <typename T>
+__device__ __forceinline__ void emit_put(const Emit<T> &e, int j, T v) {
     e.self[j] = v;
-    st_remote(e.remote + 8u * (uint32_t)j, v);
+    if constexpr (sizeof(T) == 8)
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                         e.remote + 8u * (uint32_t)j),
+                     "l"(__double_as_longlong(v)), "r"(e.rbar)
+                     : "memory");
+    else
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                         e.remote + 4u * (uint32_t)j),
+                     "r"(__float_as_uint(v)), "r"(e.rbar)
+                     : "memory");
 }
 
 // Sum of part[0..7] over the 32 lanes by recursive halving (9 shuffles, not
 // 40); every lane returns all eight totals (8 broadcast shuffles).  Lane l
 // owns total q = 4*bit4(l) + 2*bit3(l) + bit2(l) after the halving steps.
-__device__ __forceinline__ void lane_allreduce8(double (&part)[8]) {
+template <typename T>
+__device__ __forceinline__ void lane_allreduce8(T (&part)[8]) {
     const int l = threadIdx.x & 31;
-    double h4[4], h2[2], h1;
+    T h4[4], h2[2], h1;
     const bool b4 = l & 16, b3 = l & 8, b2 = l & 4;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const double mine = b4 ? part[i + 4] : part[i], other = b4 ? part[i] : part[i + 4];
+        const T mine = b4 ? part[i + 4] : part[i], other = b4 ? part[i] : part[i + 4];
         h4[i] = mine + __shfl_xor_sync(0xffffffffu, other, 16);
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-        const double mine = b3 ? h4[i + 2] : h4[i], other = b3 ? h4[i] : h4[i + 2];
+        const T mine = b3 ? h4[i + 2] : h4[i], other = b3 ? h4[i] : h4[i + 2];
         h2[i] = mine + __shfl_xor_sync(0xffffffffu, other, 8);
     }
     {
-        const double mine = b2 ? h2[1] : h2[0], other = b2 ? h2[0] : h2[1];
+        const T mine = b2 ? h2[1] : h2[0], other = b2 ? h2[0] : h2[1];
         h1 = mine + __shfl_xor_sync(0xffffffffu, other, 4);
     }
     h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
@@ -551,35 +588,36 @@ __device__ __forceinline__ void lane_allreduce8(double (&part)[8]) {
 // column dots reduce over the lanes.  carrier: column 0 is the pivot column.
 // emit: row 0 after the update (the next right op's pivot) is shipped before
 // the rest of the block is updated.
-__device__ __forceinline__ void left_apply(double (&x)[4][8], const double *p, int L, double tau,
-                                           double scale, double beta, bool carrier, const Emit &em) {
+template <typename T>
+__device__ __forceinline__ void left_apply(T (&x)[4][8], const T *p, int L, T tau,
+                                           T scale, T beta, bool carrier, const Emit<T> &em) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    double va[4], part[8];
+    T va[4], part[8];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int j = l + 32 * a;
-        va[a] = j == 0 ? 1.0 : (j < L ? p[j] * scale : 0.0);
+        va[a] = j == 0 ? T(1) : (j < L ? p[j] * scale : T(0));
     }
-    if (tau != 0.0) {                        // uniform across the CTA
+    if (tau != T(0)) {                        // uniform across the CTA
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            double t = va[0] * x[0][q];
+            T t = va[0] * x[0][q];
 #pragma unroll
             for (int a = 1; a < 4; ++a) t = fma(va[a], x[a][q], t);
             part[q] = t;
         }
-        lane_allreduce8(part);
+        lane_allreduce8<T>(part);
 #pragma unroll
         for (int q = 0; q < 8; ++q) part[q] *= tau;
     } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) part[q] = 0.0;
+        for (int q = 0; q < 8; ++q) part[q] = T(0);
     }
     if (em.self && l == 0) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) emit_put(em, w + 16 * q, fma(-part[q], va[0], x[0][q]));
     }
-    if (tau != 0.0) {
+    if (tau != T(0)) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
 #pragma unroll
@@ -587,7 +625,7 @@ __device__ __forceinline__ void left_apply(double (&x)[4][8], const double *p, i
     }
     if (carrier && w == 0) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) x[a][0] = (l + 32 * a == 0) ? beta : 0.0;
+        for (int a = 0; a < 4; ++a) x[a][0] = (l + 32 * a == 0) ? beta : T(0);
     }
 }
 
@@ -595,20 +633,21 @@ __device__ __forceinline__ void left_apply(double (&x)[4][8], const double *p, i
 // row: row dots reduce over the 16 warps through shared memory.
 // carrier: row 0 is the pivot row.  emit: column 0 after the update (the
 // next left op's pivot).
-__device__ __forceinline__ void right_apply(double (&x)[4][8], const double *p, int L, double tau,
-                                            double scale, double beta, bool carrier,
-                                            double (*red)[BK], double (*red2)[BK], const Emit &em) {
+template <typename T>
+__device__ __forceinline__ void right_apply(T (&x)[4][8], const T *p, int L, T tau,
+                                            T scale, T beta, bool carrier,
+                                            T (*red)[BK], T (*red2)[BK], const Emit<T> &em) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31, tid = threadIdx.x;
-    double vq[8], td[4];
+    T vq[8], td[4];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int c = w + 16 * q;
-        vq[q] = c == 0 ? 1.0 : (c < L ? p[c] * scale : 0.0);
+        vq[q] = c == 0 ? T(1) : (c < L ? p[c] * scale : T(0));
     }
-    if (tau != 0.0) {                        // uniform across the CTA
+    if (tau != T(0)) {                        // uniform across the CTA
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-            double t = x[a][0] * vq[0];
+            T t = x[a][0] * vq[0];
 #pragma unroll
             for (int q = 1; q < 8; ++q) t = fma(x[a][q], vq[q], t);
             red[w][l + 32 * a] = t;
@@ -626,13 +665,13 @@ __device__ __forceinline__ void right_apply(double (&x)[4][8], const double *p, 
         }
     } else {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) td[a] = 0.0;
+        for (int a = 0; a < 4; ++a) td[a] = T(0);
     }
     if (em.self && w == 0) {
 #pragma unroll
         for (int a = 0; a < 4; ++a) emit_put(em, l + 32 * a, fma(-td[a], vq[0], x[a][0]));
     }
-    if (tau != 0.0) {
+    if (tau != T(0)) {
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -640,7 +679,7 @@ __device__ __forceinline__ void right_apply(double (&x)[4][8], const double *p, 
     }
     if (carrier && l == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[0][q] = (w + 16 * q == 0) ? beta : 0.0;
+        for (int q = 0; q < 8; ++q) x[0][q] = (w + 16 * q == 0) ? beta : T(0);
     }
 }
 
@@ -654,15 +693,15 @@ __device__ __forceinline__ int msg_index(const int (&mc)[NC], int k) {
     return base + k / NC - (dr == 0 ? 1 : 0);
 }
 
-template <int NC>
-__global__ void __launch_bounds__(NTH, 1) k_chase2(double *band, int64_t n, int b, int64_t ld,
+template <int NC, typename T>
+__global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, int64_t ld,
                                                   int64_t batch, int *flags, int fstride,
-                                                  int64_t nitems, unsigned long long *trace) {
-    __shared__ double piv_self[BK];
-    __shared__ double piv0[BK];
-    __shared__ double piv_in[2][BK];
-    __shared__ double red[NW][BK];
-    __shared__ double red2[4][BK];
+                                                  int64_t nitems, unsigned long long *trace, int strict) {
+    __shared__ T piv_self[BK];
+    __shared__ T piv0[BK];
+    __shared__ T piv_in[2][BK];
+    __shared__ T red[NW][BK];
+    __shared__ T red2[4][BK];
     __shared__ __align__(8) uint64_t mbar[2];
     const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
     const unsigned rank = cluster_rank();
@@ -678,14 +717,14 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(double *band, int64_t n, int 
     const int64_t cid = blockIdx.x / NC, ncl = gridDim.x / NC;
     for (int64_t item = cid; item < nitems; item += ncl) {
         const int64_t s = item / batch, m = item % batch;
-        const Band A{band + m * n * ld, n, ld, b};
+        const BandT<T> A{band + m * n * ld, n, ld, b};
         int *fl = flags + (m * n + s) * (int64_t)fstride;     // fl[j]: block j stored
         const int nops = chase_nops(s, n, b);
         const int nprev = s > 0 ? chase_nops(s - 1, n, b) : 0;
         for (int k = (int)rank; k < nops; k += NC) {
             const Blk g = geom(s, k, n, b);
             unsigned long long *tr =
-                (trace && m == 0 && s < 256 && k < 32 && tid == 0) ? trace + (s * 32 + k) * 8 : nullptr;
+                (trace && m == 0 && s < 256 && k < 32 && tid == 0) ? trace + (s * 32 + k) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
             if (s > 0) {
                 // sweep s-1 must have stored blocks 0..k (flag 2) and the
@@ -695,7 +734,7 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(double *band, int64_t n, int 
                 const int lo = k >= NC ? k - NC + 1 : 0;
                 const int j = lo + tid;
                 if (j < min(k + 3, nprev)) {
-                    const int want = j <= k ? 2 : 1;
+                    const int want = (j <= k || strict) ? 2 : 1;
                     const int *f = fl - fstride + j;
                     for (int spin = 0; ld_acquire(f) < want; ++spin)
                         if (spin > 64) __nanosleep(32);
@@ -703,48 +742,60 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(double *band, int64_t n, int 
                 __syncthreads();
             }
             if (tr) tr[1] = gtimer();
-            double x[4][8];
-            load_blk(A, g, x);
-            const double *pv;
+            T x[4][8];
+            load_blk<T>(A, g, x);
+            const T *pv;
             int L;
             if (k == 0) {
                 L = (int)min((int64_t)b, n - s - 1);
-                for (int j = tid; j < BK; j += NTH) piv0[j] = j < L ? __ldcg(A.at(s, s + 1 + j)) : 0.0;
+                for (int j = tid; j < BK; j += NTH) piv0[j] = j < L ? __ldcg(A.at(s, s + 1 + j)) : T(0);
                 __syncthreads();
                 pv = piv0;
             } else {
                 const int idx = msg_index<NC>(mc, k);
+                if (tid == 0)       // this phase completes when the 1 KB pivot has landed
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                     saddr(&mbar[idx & 1])),
+                                 "n"(BK * (int)sizeof(T))
+                                 : "memory");
                 wait_local(saddr(&mbar[idx & 1]), (uint32_t)((idx >> 1) & 1));
                 if (tr) tr[2] = gtimer();
                 pv = piv_in[idx & 1];
                 const Blk gp = geom(s, k - 1, n, b);
                 L = (k & 1) ? gp.nr : gp.nc;
             }
-            double tau, scale, beta;
-            reflector(pv, L, tau, scale, beta);
+            if (tr) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) { if constexpr (sizeof(T) == 8) asm volatile("" ::"d"(x[a][q])); else asm volatile("" ::"f"(x[a][q])); }
+                tr[8] = gtimer();
+            }
+            T tau, scale, beta;
+            reflector<T>(pv, L, tau, scale, beta);
+            if (tr) tr[9] = gtimer();
             if (k == 0 && tid == 0) __stcg(A.at(s, s + 1), beta);
             // op k on the new block; its update yields op k+1's pivot, which is
             // shipped to the CTA holding block k+1 before the bulk update
-            Emit em{nullptr, 0u};
-            int idx1 = 0, dr = 0;
+            Emit<T> em{nullptr, 0u, 0u};
             if (k + 1 < nops) {
-                dr = (k + 1) % NC;
-                idx1 = msg_index<NC>(mc, k + 1);
+                const int dr = (k + 1) % NC;
+                const int idx1 = msg_index<NC>(mc, k + 1);
                 em.self = piv_self;
                 em.remote = mapa(saddr(&piv_in[idx1 & 1][0]), (uint32_t)dr);
+                em.rbar = mapa(saddr(&mbar[idx1 & 1]), (uint32_t)dr);
             }
-            if (k & 1) left_apply(x, pv, L, tau, scale, beta, false, em);
-            else right_apply(x, pv, L, tau, scale, beta, false, red, red2, em);
+            if (k & 1) left_apply<T>(x, pv, L, tau, scale, beta, false, em);
+            else right_apply<T>(x, pv, L, tau, scale, beta, false, red, red2, em);
             if (tr) tr[3] = gtimer();
             if (k + 1 < nops) {
-                __syncthreads();                        // piv_self / remote writes done
-                if (tid == 0) arrive_remote(mapa(saddr(&mbar[idx1 & 1]), (uint32_t)dr));
+                __syncthreads();                        // piv_self complete
                 if (tr) tr[4] = gtimer();
                 const int L1 = (k & 1) ? g.nc : g.nr;
-                reflector(piv_self, L1, tau, scale, beta);
-                const Emit none{nullptr, 0u};
-                if (k & 1) right_apply(x, piv_self, L1, tau, scale, beta, true, red, red2, none);
-                else left_apply(x, piv_self, L1, tau, scale, beta, true, none);
+                reflector<T>(piv_self, L1, tau, scale, beta);
+                const Emit<T> none{nullptr, 0u, 0u};
+                if (k & 1) right_apply<T>(x, piv_self, L1, tau, scale, beta, true, red, red2, none);
+                else left_apply<T>(x, piv_self, L1, tau, scale, beta, true, none);
             }
             if (tr) tr[5] = gtimer();
             // publish block k: its edge (row 0 of an even / Q-type block,
@@ -752,14 +803,14 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(double *band, int64_t n, int 
             // block k-2 / k-1 reads) first, then the rest
             {
                 const bool row_edge = !(k & 1);
-                store_blk(A, g, x, row_edge ? 1 : 2);
+                store_blk<T>(A, g, x, row_edge ? 1 : 2);
                 __syncthreads();
                 if (tid == 0) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     if (tr) tr[6] = gtimer();
                     st_relaxed(fl + k, 1);
                 }
-                store_blk(A, g, x, row_edge ? 3 : 4);
+                store_blk<T>(A, g, x, row_edge ? 3 : 4);
                 __syncthreads();
                 if (tid == 0) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -786,31 +837,15 @@ size_t chase_workspace_bytes(int64_t n, int bw, int64_t batch) {
     return (size_t)batch * (size_t)n * ((size_t)ld * sizeof(double) + sizeof(int)) + flags + 512;
 }
 
-template <typename S>
-cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64_t batch,
-                               int64_t a_bstride, double *d, double *e, void *ws,
-                               cudaStream_t st) {
-    if (n < 1 || batch < 1) return cudaSuccess;
-    const int b = bw;
-    const int64_t ld = 3 * (int64_t)b + 1;
-    double *band = (double *)ws;
-    int *progress = (int *)(band + batch * n * ld);
-    cudaError_t err = cudaMemsetAsync(band, 0, (size_t)batch * n * ld * sizeof(double), st);
-    if (err != cudaSuccess) return err;
-    err = cudaMemsetAsync(progress, 0, (size_t)batch * n * sizeof(int), st);
-    if (err != cudaSuccess) return err;
-    {
-        const int64_t total = n * (int64_t)(bw + 1);
-        dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 4096), (unsigned)batch);
-        k_pack_band<S><<<grid, 256, 0, st>>>(a, n, lda, a_bstride, bw, band, ld, b);
-        bsvd_host::count_launch();
-        if ((err = cudaGetLastError()) != cudaSuccess) return err;
-    }
-    if (n > 2 && b > 64 && b <= ch2::BK && !getenv("BSVD_CHASE_V1")) {
+// Carried-block cluster chase on a packed band of element type T (k_chase2).
+template <typename T>
+static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t batch, int *progress,
+                                 cudaStream_t st) {
+    cudaError_t err;
         // carried-block cluster pipeline (NC CTAs per sweep, 1 CTA per SM)
-        int NC = 3;
+        int NC = 4;
         if (const char *e = getenv("BSVD_CHASE_NC")) NC = atoi(e);
-        if (NC < 2 || NC > 4) NC = 3;
+        if (NC < 2 || NC > 4) NC = 4;
         const int64_t nitems = (n - 2) * batch;
         const int64_t nops0 = 1 + 2 * ((n - 2 + b) / b);
         int64_t want = std::min<int64_t>(nitems, batch * (nops0 / 4 + 2));
@@ -825,8 +860,8 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         lc.stream = st;
         lc.attrs = attr;
         lc.numAttrs = 1;
-        void (*kern)(double *, int64_t, int, int64_t, int64_t, int *, int, int64_t, unsigned long long *) =
-            NC == 2 ? ch2::k_chase2<2> : (NC == 4 ? ch2::k_chase2<4> : ch2::k_chase2<3>);
+        void (*kern)(T *, int64_t, int, int64_t, int64_t, int *, int, int64_t, unsigned long long *, int) =
+            NC == 2 ? ch2::k_chase2<2, T> : (NC == 3 ? ch2::k_chase2<3, T> : ch2::k_chase2<4, T>);
         int max_clusters = 0;
         lc.gridDim = dim3((unsigned)(want * NC));
         err = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &lc);
@@ -837,7 +872,7 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         int b_ = b;
         const char *trace_path = getenv("BSVD_CHASE_TRACE");
         unsigned long long *trace = nullptr;
-        const size_t trace_bytes = 256 * 32 * 8 * sizeof(unsigned long long);
+        const size_t trace_bytes = 256 * 32 * 16 * sizeof(unsigned long long);
         if (trace_path) {
             cudaMallocAsync((void **)&trace, trace_bytes, st);
             cudaMemsetAsync(trace, 0, trace_bytes, st);
@@ -846,7 +881,8 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         const int fstride = chase_max_ops(n, b);
         err = cudaMemsetAsync(flags, 0, (size_t)batch * n * fstride * sizeof(int), st);
         if (err != cudaSuccess) return err;
-        err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, flags, fstride, nitems, trace);
+        const int strict = getenv("BSVD_CHASE_STRICT") ? 1 : 0;
+        err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, flags, fstride, nitems, trace, strict);
         bsvd_host::count_launch();
         if (err != cudaSuccess) return err;
         if (trace) {
@@ -857,6 +893,59 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
             if (f) { fwrite(h.data(), 1, trace_bytes, f); fclose(f); }
             cudaFreeAsync(trace, st);
         }
+    return cudaSuccess;
+}
+
+template <typename S>
+cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64_t batch,
+                               int64_t a_bstride, double *d, double *e, void *ws,
+                               cudaStream_t st) {
+    if (n < 1 || batch < 1) return cudaSuccess;
+    const int b = bw;
+    const int64_t ld = 3 * (int64_t)b + 1;
+    if (n > 2 && b > 64 && b <= ch2::BK && !getenv("BSVD_CHASE_V1")) {
+        // carried-block cluster chase, in the compute precision of the input
+        // (fp32 for FP32 / FP16 storage like the reference's chase,
+        // secondstage.py:456-457; BSVD_CHASE_F64=1 keeps fp64)
+        const bool f32 = sizeof(S) < 8 && !getenv("BSVD_CHASE_F64");
+        const size_t es = f32 ? sizeof(float) : sizeof(double);
+        char *bandp = (char *)ws;
+        int *progress = (int *)(bandp + (size_t)batch * n * ld * es);
+        cudaError_t err = cudaMemsetAsync(bandp, 0, (size_t)batch * n * ld * es, st);
+        if (err != cudaSuccess) return err;
+        const int64_t total = n * (int64_t)(bw + 1);
+        dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 4096), (unsigned)batch);
+        dim3 g2((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch);
+        if (f32) {
+            k_pack_band<S, float><<<grid, 256, 0, st>>>(a, n, lda, a_bstride, bw, (float *)bandp, ld, b);
+            bsvd_host::count_launch();
+            if ((err = cudaGetLastError()) != cudaSuccess) return err;
+            if ((err = launch_chase2<float>((float *)bandp, n, b, ld, batch, progress, st)) != cudaSuccess) return err;
+            k_extract_bidiag<float><<<g2, 256, 0, st>>>((const float *)bandp, n, ld, b, d, e);
+        } else {
+            k_pack_band<S, double><<<grid, 256, 0, st>>>(a, n, lda, a_bstride, bw, (double *)bandp, ld, b);
+            bsvd_host::count_launch();
+            if ((err = cudaGetLastError()) != cudaSuccess) return err;
+            if ((err = launch_chase2<double>((double *)bandp, n, b, ld, batch, progress, st)) != cudaSuccess) return err;
+            k_extract_bidiag<double><<<g2, 256, 0, st>>>((const double *)bandp, n, ld, b, d, e);
+        }
+        bsvd_host::count_launch();
+        return cudaGetLastError();
+    }
+    double *band = (double *)ws;
+    int *progress = (int *)(band + batch * n * ld);
+    cudaError_t err = cudaMemsetAsync(band, 0, (size_t)batch * n * ld * sizeof(double), st);
+    if (err != cudaSuccess) return err;
+    err = cudaMemsetAsync(progress, 0, (size_t)batch * n * sizeof(int), st);
+    if (err != cudaSuccess) return err;
+    {
+        const int64_t total = n * (int64_t)(bw + 1);
+        dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 4096), (unsigned)batch);
+        k_pack_band<S, double><<<grid, 256, 0, st>>>(a, n, lda, a_bstride, bw, band, ld, b);
+        bsvd_host::count_launch();
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    if (false) {
     } else if (n > 2 && b <= 64 && batch >= 512 && !getenv("BSVD_CHASE_PIPELINED")) {
         int dev = 0, nsm = 0, per_sm = 0;
         cudaGetDevice(&dev);
@@ -931,7 +1020,7 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
         }
     }
     dim3 g2((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch);
-    k_extract_bidiag<<<g2, 256, 0, st>>>(band, n, ld, b, d, e);
+    k_extract_bidiag<double><<<g2, 256, 0, st>>>(band, n, ld, b, d, e);
     bsvd_host::count_launch();
     return cudaGetLastError();
 }

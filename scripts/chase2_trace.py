@@ -1,14 +1,20 @@
 """Summarise BSVD_CHASE_TRACE of the carried-block chase (k_chase2; development aid)."""
 import sys
 import numpy as np
-t = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(256, 32, 8).astype(np.int64)
+t = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(256, 32, 16).astype(np.int64)
 ok = (t[:, :, 0] > 0) & (t[:, :, 7] > 0) & (t[:, :, 2] > 0) & (t[:, :, 4] > 0)
 ok[:, 0] = False
 names = ["dep wait", "msg wait", "new apply", "send", "carrier apply", "store+fence", "ordered rel"]
-d = np.diff(t, axis=2)
+d = np.diff(t[:, :, :8], axis=2)
 for i, nm in enumerate(names):
     v = d[:, :, i][ok]
     print(f"{nm:14s} median {np.median(v)/1e3:7.2f} us  mean {v.mean()/1e3:7.2f} us")
+v = (t[:, :, 8] - t[:, :, 2])[ok]
+print("loads done after msg: median %.2f us (negative: before)" % (np.median(v) / 1e3))
+v = (t[:, :, 9] - np.maximum(t[:, :, 8], t[:, :, 2]))[ok]
+print("reflector: median %.2f us" % (np.median(v) / 1e3))
+v = (t[:, :, 3] - t[:, :, 9])[ok]
+print("apply (dots+emit+update): median %.2f us" % (np.median(v) / 1e3))
 # chain link: send(k+1) - send(k) within a sweep (steady part)
 link = (t[:, 2:31, 4] - t[:, 1:30, 4])
 lk = link[(t[:, 2:31, 4] > 0) & (t[:, 1:30, 4] > 0)]

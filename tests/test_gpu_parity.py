@@ -224,18 +224,21 @@ def test_large_batch_paths(P, be_tree, oracle, n, ts):
         assert_close(got[i], oracle.svdvals(a[i].T.copy(), ts), np.float32, n, what=f"member {i}")
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("n", [3, 5, 127, 128, 129, 200, 256, 257, 300, 385, 640])
-def test_chase_wide_band(P, be_tree, oracle, n):
+def test_chase_wide_band(P, be_tree, oracle, n, dtype):
     """Band width 128 runs the carried-block cluster chase (stage2_chase.cu
-    ch2): ragged tails (n not a multiple of b), blocks clipped to one row or
-    column, and sweeps shorter than the cluster."""
+    ch2), fp64 for FP64 storage and fp32 otherwise: ragged tails (n not a
+    multiple of b), blocks clipped to one row or column, and sweeps shorter
+    than the cluster."""
     rng = np.random.default_rng(n)
     a = np.triu(rng.standard_normal((n, n)))
     a -= np.triu(a, 129)
+    a = a.astype(dtype)
     d, e = P.band_to_bidiagonal(a, 128, backend=be_tree)
     got = oracle.bidiagonal_values(d, e)
-    want = np.linalg.svd(a, compute_uv=False)
-    assert_close(got, want, np.float64, n, what=f"chase b=128 n={n}")
+    want = np.linalg.svd(a.astype(np.float64), compute_uv=False)
+    assert_close(got, want, dtype, n, what=f"chase b=128 n={n} {np.dtype(dtype).name}")
 
 
 def test_chase_wide_band_batched(P, be_tree, oracle):
