@@ -15,6 +15,8 @@
 // for representable inputs.  Only the largest n_out values are computed (the
 // zero padding adds the smallest ones, matrix.py:163-181), already in the
 // descending order secondstage.py:506 produces with a sort.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -106,14 +108,109 @@ __device__ __forceinline__ void negcount2(const double *__restrict__ o2, int64_t
     c1 = n1;
 }
 
+// Sturm count (identical arithmetic to negcount) plus the Laguerre sums at x:
+// G = sum 1/(x - lambda) = (log|f|)', S2 = (log|f|)'' = -sum 1/(x - lambda)^2
+// for f(x) = det(TGK - x I), from the derivative recurrences of
+// q_j = -x - o2_j / q_{j-1}:  a_j = q_j'/q_j = (t_j a_{j-1} - 1)/q_j,
+// b_j = q_j''/q_j = t_j (b_{j-1} - 2 a_{j-1}^2)/q_j,  t_j = o2_j / q_{j-1}.
+__device__ __forceinline__ double rcp_fast(double v) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+    return r * fma(-v, r, 2.0);          // one Newton step: ample for a derivative
+}
+__device__ __forceinline__ int sturm_laguerre(const double *__restrict__ o2, int64_t m, double x,
+                                              double pivmin, double &G, double &S2) {
+    double q = -x;
+    if (fabs(q) < pivmin) q = (q < 0.0) ? -pivmin : pivmin;
+    int cnt = q < 0.0;
+    double a = -rcp_fast(q), bb = 0.0;
+    double g = a, h = -a * a;
+    for (int64_t j = 0; j < m; ++j) {
+        const double t = __ldg(o2 + j) / q;
+        double qn = -x - t;
+        if (fabs(qn) < pivmin) qn = (qn < 0.0) ? -pivmin : pivmin;
+        cnt += qn < 0.0;
+        const double rn = rcp_fast(qn);
+        const double an = fma(t, a, -1.0) * rn;
+        const double bn = t * fma(-2.0 * a, a, bb) * rn;
+        g += an;
+        h = fma(-an, an, h + bn);
+        q = qn;
+        a = an;
+        bb = bn;
+    }
+    G = g;
+    S2 = h;
+    return cnt;
+}
+
+// One value, bracket N(lo) < rank <= N(hi) with counts clo, chi known.  If
+// the bracket isolates the value (chi - clo == 1), Laguerre's iteration for
+// the real-rooted det(TGK - xI) (degree 2n) converges cubically and
+// monotonically toward it from inside; every iterate's Sturm count keeps the
+// bracket invariant, so a bad step only costs a bisection.  Then two probes
+// a few ulps either side of the converged iterate and a short bisection to
+// adjacent doubles give exactly the value plain bisection would return.
+__device__ __forceinline__ double finish_value(const double *__restrict__ ob, int64_t n, int64_t rank,
+                                               double lo, double hi, int64_t clo, int64_t chi,
+                                               double pivmin, double floor_) {
+    const int64_t m = 2 * n - 1;
+    if (chi - clo == 1 && hi > floor_) {
+        const double Nd = 2.0 * (double)n;
+        double x = 0.5 * (lo + hi);
+        bool conv = false;
+        for (int it = 0; it < 40; ++it) {
+            double G, S2;
+            const int64_t c = sturm_laguerre(ob, m, x, pivmin, G, S2) - n;
+            if (c < rank) lo = x; else hi = x;
+            if (!(hi - lo > 16.0 * 0x1p-52 * hi)) { conv = true; break; }
+            const double H = -S2;
+            double disc = (Nd - 1.0) * (Nd * H - G * G);
+            disc = disc > 0.0 ? disc : 0.0;
+            const double sq = sqrt(disc);
+            const double xa = x - Nd / (G + sq), xb = x - Nd / (G - sq);
+            double xn;
+            if (c < rank) xn = fmax(xa, xb);          // the value lies above x
+            else xn = fmin(xa, xb);                   // ... below (or at) x
+            // a step within rounding noise: x sits on the value (the count
+            // and the derivatives may then disagree about the side)
+            if (fabs(xn - x) <= 64.0 * 0x1p-52 * fabs(x)) { conv = true; break; }
+            if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
+            x = xn;
+        }
+        if (conv) {                                   // close the bracket around x
+            double dl = 16.0 * 0x1p-52 * fabs(x) + pivmin;
+            for (int rep = 0; rep < 4; ++rep) {
+                const double xl = x - dl, xh = x + dl;
+                if (xl > lo && xl < hi) {
+                    if (negcount(ob, m, xl, pivmin) - n < rank) lo = xl; else hi = xl;
+                }
+                if (xh > lo && xh < hi) {
+                    if (negcount(ob, m, xh, pivmin) - n < rank) lo = xh; else hi = xh;
+                }
+                if (hi - lo <= 2.5 * dl) break;
+                dl *= 16.0;
+            }
+        }
+    }
+    for (int it = 0; it < 200; ++it) {               // bisection to adjacent doubles
+        const double mid = 0.5 * (lo + hi);
+        if (!(mid > lo && mid < hi) || hi <= floor_) break;
+        const int64_t cnt = negcount(ob, m, mid, pivmin) - n;
+        if (cnt < rank) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
 // Multisection: a group of kLanes lanes owns one value; each round the lanes
 // evaluate 2*kLanes interior points of [lo, hi] (two interleaved Sturm
 // chains per lane) and keep the sub-interval where the count crosses the
-// value's rank (4.1 bits per round instead of 1, and 16x the independent
-// chains of one-thread-per-value bisection).  Once the points collapse (a
-// few ulps) the group finishes with plain bisection.  The invariant
-// N(lo) < rank <= N(hi) is the same, so the result is identical to bisection
-// to adjacent doubles.
+// value's rank (4.1 bits per round instead of 1), until the value is
+// isolated (exactly one eigenvalue in the bracket) or the points collapse.
+// With kLanes == 1 plain bisection plays that role.  finish_value then
+// converges by Laguerre's method (one lane).  The invariant
+// N(lo) < rank <= N(hi) holds throughout, so the result equals bisection to
+// adjacent doubles.
 template <int kLanes, typename OutT>
 __global__ void __launch_bounds__(128) k_bisect(const double *__restrict__ o2,
                                                 const double *__restrict__ scal, int64_t n,
@@ -133,46 +230,137 @@ __global__ void __launch_bounds__(128) k_bisect(const double *__restrict__ o2,
         const double pivmin = 0x1p-1000;
         const double floor_ = 0x1p-120 * gersh;
         double lo = 0.0, hi = 2.0 * gersh;
+        int64_t clo = 0, chi = n;                        // N(lo), N(hi)
         constexpr int NP = 2 * kLanes;                   // points per round
-        for (int round = 0; round < (kLanes > 1 ? 40 : 0); ++round) {
-            if (hi <= floor_) break;
-            const double h = (hi - lo) / (NP + 1);
-            const double x0 = lo + h * (2 * sub + 1), x1 = lo + h * (2 * sub + 2);
-            // points must be strictly increasing inside (lo, hi); else bisect
-            const bool ok = h > 0.0 && (lo + h) > lo && (lo + h * NP) < hi && x0 < x1;
-            if (!__all_sync(gmask, ok)) break;
-            int c0, c1;
-            negcount2(ob, 2 * n - 1, x0, x1, pivmin, c0, c1);
-            c0 -= (int)n;
-            c1 -= (int)n;
-            // bit t-1 of M <=> point t has N(x) < rank; lo moves to the HIGHEST such
-            // point (robust even if rounding made the computed counts non-monotone:
-            // every point above it has N >= rank, so hi = the next point).
-            const unsigned below = __ballot_sync(gmask, c0 < rank) >> (lane - sub);
-            const unsigned below1 = __ballot_sync(gmask, c1 < rank) >> (lane - sub);
-            unsigned M = 0;
+        if constexpr (kLanes > 1) {
+            for (int round = 0; round < 40; ++round) {
+                if (hi <= floor_ || chi - clo == 1) break;
+                const double h = (hi - lo) / (NP + 1);
+                const double x0 = lo + h * (2 * sub + 1), x1 = lo + h * (2 * sub + 2);
+                // points must be strictly increasing inside (lo, hi); else stop
+                const bool ok = h > 0.0 && (lo + h) > lo && (lo + h * NP) < hi && x0 < x1;
+                if (!__all_sync(gmask, ok)) break;
+                int c0, c1;
+                negcount2(ob, 2 * n - 1, x0, x1, pivmin, c0, c1);
+                c0 -= (int)n;
+                c1 -= (int)n;
+                // bit t-1 of M <=> point t has N(x) < rank; lo moves to the HIGHEST such
+                // point (robust even if rounding made the computed counts non-monotone:
+                // every point above it has N >= rank, so hi = the next point).
+                const unsigned below = __ballot_sync(gmask, c0 < rank) >> (lane - sub);
+                const unsigned below1 = __ballot_sync(gmask, c1 < rank) >> (lane - sub);
+                unsigned M = 0;
 #pragma unroll
-            for (int s = 0; s < kLanes; ++s)
-                M |= (((below >> s) & 1u) << (2 * s)) | (((below1 >> s) & 1u) << (2 * s + 1));
-            const int nb = M ? 32 - __clz(M) : 0;             // highest point index below rank
-            const double nlo = nb > 0 ? lo + h * nb : lo;
-            const double nhi = nb < NP ? lo + h * (nb + 1) : hi;
-            lo = nlo;
-            hi = nhi;
+                for (int s = 0; s < kLanes; ++s)
+                    M |= (((below >> s) & 1u) << (2 * s)) | (((below1 >> s) & 1u) << (2 * s + 1));
+                const int nb = M ? 32 - __clz(M) : 0;             // highest point index below rank
+                // counts at the new ends: point t is chain (t-1)&1 of lane (t-1)>>1
+                const int base = lane - sub;
+                const int tl = nb > 0 ? nb - 1 : 0, th = nb < NP ? nb : 0;
+                const int l0 = __shfl_sync(gmask, c0, base + (tl >> 1)), l1 = __shfl_sync(gmask, c1, base + (tl >> 1));
+                const int h0 = __shfl_sync(gmask, c0, base + (th >> 1)), h1 = __shfl_sync(gmask, c1, base + (th >> 1));
+                if (nb > 0) clo = (tl & 1) ? l1 : l0;
+                if (nb < NP) chi = (th & 1) ? h1 : h0;
+                const double nlo = nb > 0 ? lo + h * nb : lo;
+                const double nhi = nb < NP ? lo + h * (nb + 1) : hi;
+                lo = nlo;
+                hi = nhi;
+            }
+        } else {
+            for (int it = 0; it < 64; ++it) {               // bisect until isolated
+                if (hi <= floor_ || chi - clo == 1) break;
+                const double mid = 0.5 * (lo + hi);
+                if (!(mid > lo && mid < hi)) break;
+                const int64_t cnt = negcount(ob, 2 * n - 1, mid, pivmin) - n;
+                if (cnt < rank) { lo = mid; clo = cnt; } else { hi = mid; chi = cnt; }
+            }
         }
-        for (int it = 0; it < 200; ++it) {               // finish: bisection to adjacent doubles
-            const double mid = 0.5 * (lo + hi);
-            if (!(mid > lo && mid < hi) || hi <= floor_) break;
-            const int cnt = negcount(ob, 2 * n - 1, mid, pivmin) - (int)n;
-            if (cnt < rank) lo = mid; else hi = mid;
-        }
-        res = lo * unscale;
+        if (sub == 0) res = finish_value(ob, n, rank, lo, hi, clo, chi, pivmin, floor_) * unscale;
     }
     if (active && sub == 0) out[b * out_stride + k] = (OutT)res;
 }
 
+// Spectrum slicing: Sturm counts at P uniform points x_p = p h of
+// (0, 2 gersh], two interleaved chains per thread.  cnt[p] = N(x_p) =
+// #{sigma < x_p}; one count serves every value (a value's cell is found by
+// binary search), so isolating n values costs P counts instead of ~n log.
+__global__ void __launch_bounds__(128) k_slice(const double *__restrict__ o2,
+                                               const double *__restrict__ scal, int64_t n, int P,
+                                               int *__restrict__ cnt) {
+    const int64_t b = blockIdx.y;
+    const double *ob = o2 + b * (2 * n - 1);
+    int *cb = cnt + b * (int64_t)(P + 1);
+    const double gersh = scal[2 * b + 1];
+    const double h = 2.0 * gersh / P;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (2 * i + 1 > P) return;
+    if (i == 0) cb[0] = 0;
+    if (!(gersh > 0.0)) {
+        cb[2 * i + 1] = (int)n;
+        if (2 * i + 2 <= P) cb[2 * i + 2] = (int)n;
+        return;
+    }
+    const double pivmin = 0x1p-1000;
+    const int p0 = 2 * i + 1, p1 = min(2 * i + 2, P);
+    int c0, c1;
+    negcount2(ob, 2 * n - 1, p0 * h, p1 * h, pivmin, c0, c1);
+    cb[p0] = c0 - (int)n;
+    if (p1 != p0) cb[p1] = c1 - (int)n;
+}
+
+// One thread per value: its cell from the slice counts (binary search for
+// the first x_p with N(x_p) >= rank), bisection until the value is isolated,
+// then finish_value (Laguerre + probes + bisection to adjacent doubles).
+template <typename OutT>
+__global__ void __launch_bounds__(128) k_values(const double *__restrict__ o2,
+                                                const double *__restrict__ scal,
+                                                const int *__restrict__ cnt, int P, int64_t n,
+                                                int64_t n_out, OutT *__restrict__ out,
+                                                int64_t out_stride) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    if (k >= n_out) return;
+    const double *ob = o2 + b * (2 * n - 1);
+    const int *cb = cnt + b * (int64_t)(P + 1);
+    const double unscale = scal[2 * b], gersh = scal[2 * b + 1];
+    const int64_t rank = n - k;
+    double res = 0.0;
+    if (gersh > 0.0) {
+        const double pivmin = 0x1p-1000;
+        const double floor_ = 0x1p-120 * gersh;
+        const double h = 2.0 * gersh / P;
+        int lo_p = 0, hi_p = P;                          // cb[lo_p] < rank <= cb[hi_p]
+        while (hi_p - lo_p > 1) {
+            const int mid = (lo_p + hi_p) >> 1;
+            if (__ldg(cb + mid) < rank) lo_p = mid; else hi_p = mid;
+        }
+        double lo = lo_p * h, hi = hi_p < P ? hi_p * h : 2.0 * gersh;
+        int64_t clo = __ldg(cb + lo_p), chi = __ldg(cb + hi_p);
+        if (!(clo < rank && rank <= chi)) {              // non-monotone counts: full range
+            lo = 0.0; hi = 2.0 * gersh; clo = 0; chi = n;
+        }
+        for (int it = 0; it < 64; ++it) {                // bisect until isolated
+            if (hi <= floor_ || chi - clo == 1) break;
+            const double mid = 0.5 * (lo + hi);
+            if (!(mid > lo && mid < hi)) break;
+            const int64_t c = negcount(ob, 2 * n - 1, mid, pivmin) - n;
+            if (c < rank) { lo = mid; clo = c; } else { hi = mid; chi = c; }
+        }
+        res = finish_value(ob, n, rank, lo, hi, clo, chi, pivmin, floor_) * unscale;
+    }
+    out[b * out_stride + k] = (OutT)res;
+}
+
+static int slice_points(int64_t n) {
+    int64_t P = 4 * n;
+    if (P < 256) P = 256;
+    if (P > 65536) P = 65536;
+    return (int)P;
+}
+
 size_t bisect_workspace_bytes(int64_t n, int64_t batch) {
-    return (size_t)batch * ((size_t)(2 * n) * sizeof(double) + 2 * sizeof(double)) + 256;
+    return (size_t)batch * ((size_t)(2 * n) * sizeof(double) + 2 * sizeof(double) +
+                            (size_t)(slice_points(n) + 1) * sizeof(int)) + 512;
 }
 
 template <typename OutT>
@@ -186,6 +374,18 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
     bsvd_host::count_launch();
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
+    if (!getenv("BSVD_BISECT_MULTI")) {
+        // spectrum slicing + one thread per value (Laguerre finish)
+        const int P = slice_points(n);
+        int *cnt = (int *)(((uintptr_t)(scal + 2 * batch) + 15) & ~(uintptr_t)15);
+        k_slice<<<dim3((unsigned)((P / 2 + 1 + 127) / 128), (unsigned)batch), 128, 0, st>>>(o2, scal, n, P, cnt);
+        bsvd_host::count_launch();
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        k_values<OutT><<<dim3((unsigned)((n_out + 127) / 128), (unsigned)batch), 128, 0, st>>>(
+            o2, scal, cnt, P, n, n_out, out, out_stride);
+        bsvd_host::count_launch();
+        return cudaGetLastError();
+    }
     // Multisection when values are scarce (one large matrix), plain bisection
     // (one lane per value, least total work) when a batch supplies the parallelism.
     if (n_out * batch >= 131072) {
