@@ -76,7 +76,11 @@ struct Lane {
 
 // acc[i][j] += sign * sum_k A[k][m0+i] * Bs[k][n0+j]; A global [TS][TS] streamed
 // in KC-row chunks through Abuf (2 x KC x TS), Bs shared [TS][BNP].
-template <typename C, int TS, typename G, bool NEG, int BNP>
+// TRI: structure of the A operand A(k, m) = Ag[k][m] -- 0 dense, 1 zero for
+// k > m, 2 zero for k < m (the triangular reflector factors).  When a K-chunk
+// lines up with a warp's row block, warps skip the chunks that are entirely
+// zero for their rows (the CTA still walks every chunk for the buffer sync).
+template <typename C, int TS, typename G, bool NEG, int BNP, int TRI = 0>
 __device__ __forceinline__ void gemm(const C *__restrict__ Ag, const C *Bs, C *Abuf,
                                      C (&acc)[G::MR][G::NR], const Lane<G> &ln) {
     constexpr int bnp = BNP;
@@ -103,8 +107,11 @@ __device__ __forceinline__ void gemm(const C *__restrict__ Ag, const C *Bs, C *A
         __syncthreads();
         const C *As = Abuf + (ch & 1) * CH;
         const C *Bk = Bs + (size_t)ch * KC * bnp;
+        constexpr bool SKIP = TRI != 0 && KC == G::BM / G::WGM;
+        const int wm = (threadIdx.x >> 5) % G::WGM;          // the warp's row block
+        const bool zero = SKIP && (TRI == 1 ? ch > wm : ch < wm);
 #pragma unroll 4
-        for (int k = 0; k < KC; ++k) {
+        for (int k = 0; k < (zero ? 0 : KC); ++k) {
             C a[G::MR], b[G::NR];
 #pragma unroll
             for (int i = 0; i < G::MR; ++i) a[i] = As[k * TS + ln.m0 + i];
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(apply::kNT) k_apply_leaf(View<S> V, int64_t to
     __syncthreads();
     C acc[G::MR][G::NR];
     zero<C, G>(acc);
-    gemm<C, TS, G, false, BNP>(Vk, Xs, Abuf, acc, ln);   // W = V^T X
+    gemm<C, TS, G, false, BNP, 2>(Vk, Xs, Abuf, acc, ln);   // W = V^T X
     to_smem<C, G>(acc, Ws, BNP, ln);
     init_from<C, G>(acc, Xs, BNP, ln);
     __syncthreads();
@@ -231,7 +238,6 @@ __global__ void __launch_bounds__(apply::kNT) k_apply_tt(View<S> V, int64_t top,
     C *Abuf = (C *)smem_raw;
     C *Xt = Abuf + 2 * KC * TS;
     C *Xb = Xt + TS * BNP;
-    C *Ws = Xb + TS * BNP;
     const int64_t b = blockIdx.z, p = blockIdx.y;
     V.base += b * a_bstride;
     nodes += b * ws_bstride;
@@ -243,16 +249,28 @@ __global__ void __launch_bounds__(apply::kNT) k_apply_tt(View<S> V, int64_t top,
     load_x<S, C, TS, G::BN>(V, rt, c0, cmax, Xt, BNP);
     load_x<S, C, TS, G::BN>(V, rb, c0, cmax, Xb, BNP);
     __syncthreads();
-    C acc[G::MR][G::NR];
-    init_from<C, G>(acc, Xt, BNP, ln);
-    gemm<C, TS, G, false, BNP>(Vk, Xb, Abuf, acc, ln);   // W = X_top + Vb^T X_bot
-    to_smem<C, G>(acc, Ws, BNP, ln);
+    // X_top's microtile stays in registers, so its shared buffer carries W
+    // and then W2 (two tiles of shared memory instead of three: 2 CTAs/SM)
+    C xt[G::MR][G::NR], acc[G::MR][G::NR];
+    init_from<C, G>(xt, Xt, BNP, ln);
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int jx = 0; jx < G::NR; ++jx) acc[i][jx] = xt[i][jx];
+    gemm<C, TS, G, false, BNP, 1>(Vk, Xb, Abuf, acc, ln);   // W = X_top + Vb^T X_bot (Vb upper)
+    to_smem<C, G>(acc, Xt, BNP, ln);                        // (gemm ended on a barrier)
     __syncthreads();
-    init_from<C, G>(acc, Xt, BNP, ln);
-    gemm<C, TS, G, true, BNP>(Tt, Ws, Abuf, acc, ln);    // X_top -= T^T W
-    store_acc<S, C, G>(V, rt, c0, cmax, acc, ln);
+    zero<C, G>(acc);
+    gemm<C, TS, G, false, BNP, 1>(Tt, Xt, Abuf, acc, ln);   // W2 = T^T W (T upper)
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int jx = 0; jx < G::NR; ++jx) xt[i][jx] -= acc[i][jx];
+    store_acc<S, C, G>(V, rt, c0, cmax, xt, ln);            // X_top -= W2
+    to_smem<C, G>(acc, Xt, BNP, ln);                        // W2 (gemm ended on a barrier)
+    __syncthreads();
     init_from<C, G>(acc, Xb, BNP, ln);
-    gemm<C, TS, G, true, BNP>(Um, Ws, Abuf, acc, ln);    // X_bot -= U W
+    gemm<C, TS, G, true, BNP, 2>(Um, Xt, Abuf, acc, ln);    // X_bot -= Vb W2 (Um = Vb^T layout)
     store_acc<S, C, G>(V, rb, c0, cmax, acc, ln);
 }
 
@@ -261,7 +279,7 @@ size_t apply_smem(bool tt) {
     using G = Geo<C, TS>;
     constexpr int BNP = G::BN + 16 / (int)sizeof(C);
     constexpr int KC = (G::KC < TS) ? G::KC : TS;
-    return (size_t)(2 * KC * TS + (tt ? 3 : 2) * TS * BNP) * sizeof(C);
+    return (size_t)(2 * KC * TS + 2 * TS * BNP) * sizeof(C);
 }
 
 // Host side: one launch for the leaves, one per tree level.

@@ -612,11 +612,11 @@ __global__ void __launch_bounds__(kNTP) k_panel_blk(View<S> V, int64_t m, int64_
                     Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
                     Tt[idx] = (r <= i) ? A[i * lda + r] : C(0);
                 }
-                // U(r, i) = sum_{jj >= max(i, r)} Vb(r, jj) T(i, jj)
-                blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
-                    [&](int r, int jj) { return jj >= r ? A[jj * lda + TS + r] : C(0); },
-                    [&](int jj, int i) { return jj >= i ? A[jj * lda + i] : C(0); },
-                    [&](int r, int i, C v) { Um[i * TS + r] = v; });
+                // TT update X_bot -= Vb (T^T W): Vb in the transposed operand layout
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {
+                    const int i = idx / TS, r = idx % TS;
+                    Um[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
+                }
                 __syncthreads();
             } else {
                 constexpr int PK = PB::PK;
@@ -652,10 +652,10 @@ __global__ void __launch_bounds__(kNTP) k_panel_blk(View<S> V, int64_t m, int64_
                     Vk[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
                     Tt[idx] = (r <= i) ? Tp[pk(r, i)] : C(0);
                 }
-                blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
-                    [&](int r, int jj) { return jj >= r ? Rb[pk(r, jj)] : C(0); },
-                    [&](int jj, int i) { return jj >= i ? Tp[pk(i, jj)] : C(0); },
-                    [&](int r, int i, C v) { Um[i * TS + r] = v; });
+                for (int idx = tid; idx < TS * TS; idx += kNTP) {   // Vb, transposed operand layout
+                    const int i = idx / TS, r = idx % TS;
+                    Um[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
+                }
                 __syncthreads();
             }
             mark(5);
@@ -762,11 +762,19 @@ __global__ void __launch_bounds__(kNTP) k_node_tu(C *nodes, int64_t slot0, int64
             [&](int r, int i, C v) { img_put<C, TS>(imU, r, i, v); });
         return;
     }
-    if (tt)
+    if (tt) {
         for (int idx = tid; idx < TS * TS; idx += kNTP) {
             const int r = idx / TS, i = idx % TS;   // Tt[r][i] = T(r, i)
             Tt[idx] = (r <= i) ? Ts[i * LD + r] : C(0);
         }
+        // TT nodes apply X_bot -= Vb (T^T W) (stage1_apply.cu): no U, but Vb
+        // in the transposed operand layout, Um[i][r] = Vb(r, i)
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int i = idx / TS, r = idx % TS;
+            Um[idx] = Vs[i * LD + r];
+        }
+        return;
+    }
     // U(r, i) = sum_{j >= i} V(r, j) T(i, j)
     blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
         [&](int r, int j) { return Vs[j * LD + r]; },
@@ -880,10 +888,11 @@ __global__ void __launch_bounds__(kNTP) k_panel_tt(View<S> V, int64_t m, int64_t
                 Vk[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
                 Tt[idx] = (r <= i) ? A[i * lda + r] : C(0);
             }
-            blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
-                [&](int r, int jj) { return jj >= r ? A[jj * lda + TS + r] : C(0); },
-                [&](int jj, int i) { return jj >= i ? A[jj * lda + i] : C(0); },
-                [&](int r, int i, C v) { Um[i * TS + r] = v; });
+            // TT update X_bot -= Vb (T^T W): Vb in the transposed operand layout
+            for (int idx = tid; idx < TS * TS; idx += kNTP) {
+                const int i = idx / TS, r = idx % TS;
+                Um[idx] = (r <= i) ? A[i * lda + TS + r] : C(0);
+            }
         }
     } else {
         constexpr int PK = PB::PK;
@@ -917,10 +926,10 @@ __global__ void __launch_bounds__(kNTP) k_panel_tt(View<S> V, int64_t m, int64_t
             Vk[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
             Tt[idx] = (r <= i) ? Tp[pk(r, i)] : C(0);
         }
-        blk::sgemm<C, 4, 4, kNTP>(TS, TS, TS,
-            [&](int r, int jj) { return jj >= r ? Rb[pk(r, jj)] : C(0); },
-            [&](int jj, int i) { return jj >= i ? Tp[pk(i, jj)] : C(0); },
-            [&](int r, int i, C v) { Um[i * TS + r] = v; });
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {   // Vb, transposed operand layout
+            const int i = idx / TS, r = idx % TS;
+            Um[idx] = (r <= i) ? Rb[pk(r, i)] : C(0);
+        }
     }
     if (gridDim.x == 1 && ((int64_t)1 << j) >= m) {   // the root level: R into the band tile
         __syncthreads();
@@ -977,11 +986,27 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if ((err = cudaStreamCreateWithPriority(&st1, cudaStreamNonBlocking, hi)) != cudaSuccess) return err;
         st = st1;
     }
+    // BSVD_S1_TRACE=k: event timeline of sweep side k (RQ) on the three streams
+    const int trace_k = getenv("BSVD_S1_TRACE") ? atoi(getenv("BSVD_S1_TRACE")) : -1;
+    std::vector<std::pair<const char *, cudaEvent_t>> tl;
+    int tl_side = -1;
+    auto tlmark = [&](const char *what, cudaStream_t s2_) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s2_);
+        tl.push_back({what, e});
+    };
     // T and U of a level on a third stream as soon as the panel level exists,
     // so they overlap the previous level's trailing update; the update of
     // level j (st2) then waits only for its own factors.
+    // (high priority: a level's factors must not queue behind the thousands
+    // of CTAs of the previous level's update)
     cudaStream_t st3;
-    if ((err = cudaStreamCreateWithFlags(&st3, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    {
+        int plo = 0, phi = 0;
+        cudaDeviceGetStreamPriorityRange(&plo, &phi);
+        if ((err = cudaStreamCreateWithPriority(&st3, cudaStreamNonBlocking, phi)) != cudaSuccess) return err;
+    }
     const int Lmax0 = tree_levels(N);
     std::vector<cudaEvent_t> tuev(Lmax0 + 1);
     for (auto &e : tuev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -995,16 +1020,22 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         cudaStreamWaitEvent(st3, (*lvlp)[j], 0);
         if ((e2 = node_tu(slot0, count, tt, st3)) != cudaSuccess) return e2;
         cudaEventRecord(tuev[j], st3);
+        if (tl_side) tlmark("  node_tu", st3);
         cudaStreamWaitEvent(st2, tuev[j], 0);
         return cudaSuccess;
     };
-    auto apply_level = [&](bool lq, int64_t top, int64_t k, int64_t m, int j) -> cudaError_t {
+    auto apply_level0 = [&](bool lq, int64_t top, int64_t k, int64_t m, int j) -> cudaError_t {
         if constexpr (sizeof(C) == 4 && TS == 128) {
             if (use_tc)
                 return launch_apply_level_tc<S>(a, n, batch, a_bstride, lq, top, k, m, (const float *)img,
                                                 ws_elems, j, st2);
         }
         return launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, j, st2);
+    };
+    auto apply_level = [&](bool lq, int64_t top, int64_t k, int64_t m, int j) -> cudaError_t {
+        const cudaError_t e3 = apply_level0(lq, top, k, m, j);
+        if (tl_side) tlmark("    apply", st2);
+        return e3;
     };
     const int Lmax = tree_levels(N);
     std::vector<cudaEvent_t> lvl(Lmax + 1);
@@ -1032,12 +1063,15 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         const bool trail = (N - 1 - k) > 0;
         Side sd{};
         cudaStreamWaitEvent(st, done, 0);
+        tl_side = (!lq && k == trace_k) ? 1 : 0;
+        if (tl_side) tlmark("start", st);
         if (timed) sd.p0 = tmark(st);
         k_panel_leaf<S, C, TS, DEFER><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, ws, ws_elems, a_bstride);
         bsvd_host::count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         cudaEventRecord(lvl[0], st);
+        if (tl_side) tlmark("panel leaf", st);
         if (trail) {
             if (timed) sd.t0 = tmark(st2);
             if ((e = level_tu(0, 0, m, false)) != cudaSuccess) return e;
@@ -1052,6 +1086,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
             cudaEventRecord(lvl[j], st);
+            if (tl_side) tlmark("panel tt", st);
             if (trail && pairs > 0) {
                 if ((e = level_tu(j, tree_offset(m, j), pairs, true)) != cudaSuccess) return e;
                 if ((e = apply_level(lq, top, k, m, j)) != cudaSuccess) return e;
@@ -1089,6 +1124,17 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
             }
         }
         for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
+    if (!tl.empty()) {
+        cudaStreamSynchronize(caller);
+        for (auto &pe : tl) {
+            float ms = 0.f;
+            cudaError_t te = cudaEventSynchronize(pe.second);
+            if (te == cudaSuccess) te = cudaEventElapsedTime(&ms, tl[0].second, pe.second);
+            fprintf(stderr, "[s1 side %d] %-12s %8.1f us %s\n", trace_k, pe.first, ms * 1e3,
+                    te == cudaSuccess ? "" : cudaGetErrorString(te));
+        }
+        for (auto &pe : tl) cudaEventDestroy(pe.second);
     }
     for (auto &e : lvl) cudaEventDestroy(e);
     for (auto &e : tuev) cudaEventDestroy(e);
