@@ -70,6 +70,19 @@ __global__ void __launch_bounds__(256) k_bisect_prep(const double *__restrict__ 
     }
 }
 
+// o / q for the Sturm recurrences: reciprocal seed, two Newton steps and one
+// residual correction (the arithmetic of the IEEE division's fast path, but
+// branch-free: the recurrence's operands never reach its slow-path ranges --
+// |q| >= pivmin = 2^-1000, o <= 4 after prescaling).
+__device__ __forceinline__ double sdiv(double o, double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    r = r * fma(-q, r, 2.0);
+    r = r * fma(-q, r, 2.0);
+    const double y = o * r;
+    return fma(fma(-q, y, o), r, y);
+}
+
 // #{eigenvalues of TGK < x} for the scaled problem (LAPACK dstebz-style
 // negcount with a pivot floor; zero diagonal so a_j - x = -x).
 __device__ __forceinline__ int negcount(const double *__restrict__ o2, int64_t m, double x,
@@ -81,7 +94,7 @@ __device__ __forceinline__ int negcount(const double *__restrict__ o2, int64_t m
     if (fabs(q) < pivmin) q = (q < 0.0) ? -pivmin : pivmin;
     int cnt = q < 0.0;
     for (int64_t j = 0; j < m; ++j) {
-        q = -x - __ldg(o2 + j) / q;
+        q = -x - sdiv(__ldg(o2 + j), q);
         if (fabs(q) < pivmin) q = (q < 0.0) ? -pivmin : pivmin;
         cnt += q < 0.0;
     }
@@ -97,8 +110,8 @@ __device__ __forceinline__ void negcount2(const double *__restrict__ o2, int64_t
     int n0 = q0 < 0.0, n1 = q1 < 0.0;
     for (int64_t j = 0; j < m; ++j) {
         const double o = __ldg(o2 + j);
-        q0 = -x0 - o / q0;
-        q1 = -x1 - o / q1;
+        q0 = -x0 - sdiv(o, q0);
+        q1 = -x1 - sdiv(o, q1);
         if (fabs(q0) < pivmin) q0 = (q0 < 0.0) ? -pivmin : pivmin;
         if (fabs(q1) < pivmin) q1 = (q1 < 0.0) ? -pivmin : pivmin;
         n0 += q0 < 0.0;
@@ -126,7 +139,7 @@ __device__ __forceinline__ int sturm_laguerre(const double *__restrict__ o2, int
     double a = -rcp_fast(q), bb = 0.0;
     double g = a, h = -a * a;
     for (int64_t j = 0; j < m; ++j) {
-        const double t = __ldg(o2 + j) / q;
+        const double t = sdiv(__ldg(o2 + j), q);
         double qn = -x - t;
         if (fabs(qn) < pivmin) qn = (qn < 0.0) ? -pivmin : pivmin;
         cnt += qn < 0.0;
