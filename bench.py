@@ -253,32 +253,41 @@ def run_b200(args):
     dom = max(walls, key=walls.get)
     bw = cfg.tilesize
     npad = -(-n // bw) * bw
-    if dom == "stage1":
-        fpk = fp64_peak if dtype == torch.float64 else fp32_peak
-        ach = flop_model(n) * units / (stage1_ms * 1e-3) / 1e12
-        roof = {"bound": "fma", "kernel": "stage 1 (k_panel_leaf/k_panel_tt + k_apply_leaf/k_apply_tt, overlapped)",
-                "achieved": ach, "peak": fpk, "unit": "TFLOP/s", "frac": ach / fpk,
-                "peak_source": f"derived {'FP64' if dtype == torch.float64 else 'FP32'} FMA peak "
-                               f"148 SMs x 128 lanes x 2 x {smax:.0f} MHz (no FP32-FMA entry in MEASURED_PEAKS.json)",
-                "traffic": None}
-    elif dom == "bidiagonal":
-        algo_bytes = 2.0 * bw * npad * npad * 8 * units
-        ach = algo_bytes / (per["bidiagonal"] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "k_chase (stage 2, L2-resident band)",
-                "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
-                "peak_source": peak_src, "algorithmic_bytes": algo_bytes,
-                "model": "touch model 2*bw*n^2*8 B per matrix (SURVEY.md 8(d))", "traffic": None}
-    else:
-        iters = 64
-        algo_flops = units * n * iters * 2 * npad * 2.0
-        ach = algo_flops / (per["diagonal"] * 1e-3) / 1e12
-        roof = {"bound": "fma", "kernel": "k_bisect (stage 3)", "achieved": ach, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": ach / fp64_peak, "peak_source": "derived FP64 FMA peak",
-                "traffic": None}
+    fpk = fp64_peak if dtype == torch.float64 else fp32_peak
+    fpk_src = (f"derived {'FP64' if dtype == torch.float64 else 'FP32'} FMA peak 148 SMs x "
+               f"{64 if dtype == torch.float64 else 128} lanes x 2 x {smax:.0f} MHz "
+               "(MEASURED_PEAKS.json has no CUDA-core FMA entry)")
+    ach1 = flop_model(n) * units / (stage1_ms * 1e-3) / 1e12
+    phases = {
+        "stage1": {"bound": "fma", "kernel": "stage 1 (k_panel_leaf/k_panel_tt + k_node_tu + k_apply_leaf/k_apply_tt on 3 streams)",
+                   "achieved": ach1, "peak": fpk, "unit": "TFLOP/s", "frac": ach1 / fpk,
+                   "peak_source": fpk_src, "model": "8/3 n^3 flops (the reference's count)", "traffic": None},
+    }
+    # stage 2 chases in the compute precision (fp32 band for FP32/FP16, fp64 for FP64)
+    belem = 8 if dtype == torch.float64 else 4
+    algo_bytes = 2.0 * bw * npad * npad * belem * units
+    ach2 = algo_bytes / (per["bidiagonal"] * 1e-3) / 1e9
+    phases["bidiagonal"] = {"bound": "hbm", "kernel": "k_chase2 (stage 2, carried-block cluster chase, one launch)",
+                            "achieved": ach2, "peak": hbm_gbs, "unit": "GB/s", "frac": ach2 / hbm_gbs,
+                            "peak_source": peak_src, "algorithmic_bytes": algo_bytes,
+                            "model": f"touch model 2*bw*n^2*{belem} B per matrix (SURVEY.md 8(d))", "traffic": None}
+    # stage 3: counted Sturm steps are not fixed; report time against the FP64 pipe
+    # on a 64-count-per-value model of plain bisection (the work it replaces)
+    algo3 = units * n * 64 * 2 * npad * 10.0
+    ach3 = algo3 / (per["diagonal"] * 1e-3) / 1e12
+    phases["diagonal"] = {"bound": "fma", "kernel": "k_slice + k_values (stage 3)", "achieved": ach3,
+                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach3 / fp64_peak,
+                          "peak_source": "derived FP64 FMA peak",
+                          "model": "64 Sturm counts x 2n steps x 10 flops per value (bisection-equivalent)",
+                          "traffic": None}
+    roof = dict(phases[dom])
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
-            roof["traffic"] = json.load(open(prof)).get(roof["kernel"].split()[0])
+            tr = json.load(open(prof))
+            roof["traffic"] = tr.get(roof["kernel"].split()[0])
+            for ph in phases.values():
+                ph["traffic"] = tr.get(ph["kernel"].split()[0])
         except Exception:
             pass
 
@@ -300,7 +309,8 @@ def run_b200(args):
                        "l2": "inputs larger than L2 (the padded working copy is rewritten every step)"},
             "stages_ms": per, "stage1_wall_ms": stage1_ms,
             "stage1_tflops": flop_model(n) * units / (stage1_ms * 1e-3) / 1e12,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "phase_roofline": phases, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
