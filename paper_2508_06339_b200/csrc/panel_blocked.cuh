@@ -102,66 +102,55 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
         C x[RPW];
 #pragma unroll
         for (int q = 0; q < RPW; ++q) x[q] = (c < NB) ? A[(J0 + c) * lda + row(i0 + q)] : C(0);
-        // red: sig_part[NWF] | alpha | pad | dpart[NWF*32] | vbuf[R] (this warp's slab of v)
+        // red: sig_part[NWF] | alpha | pad | dpart[NWF*32] | vbuf[R] (this warp's slab:
+        // the pivot column at the start of a step, then v)
         C *sig_part = red, *alpha_s = red + NWF, *dpart = red + NWF + 2;
         C *vbuf = dpart + NWF * 32 + i0;
+        static_assert(RPW <= 32, "one lane per row of the warp's slab");
+        if (c == 0) {
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) vbuf[q] = x[q];
+        }
         for (int kl = 0; kl < NB; ++kl) {
             // row-list index i is on reflector kl (excluding its unit row kl)?
             auto on_ref = [&](int i) { return TT ? (i >= NB && i - NB <= J0 + kl) : (i > kl); };
-#ifdef BSVD_QR_PROBE
-            const bool probe = st && J0 == 0 && kl == 5 && threadIdx.x == 64;
-#define PROBE(k) if (probe) st[200 + (k)] = stamp_now();
-#else
-#define PROBE(k)
-#endif
-            PROBE(0)
-            if (c == kl) {
-                C s0 = C(0), s1 = C(0);
+            __syncwarp();
+            // lane q < RPW owns row i0 + q of the pivot column (published by lane kl):
+            // the norm and v are formed lane-parallel instead of by the pivot lane alone
+            const int ic = i0 + c;
+            const bool mine = c < RPW;
+            const C xv = mine ? vbuf[c] : C(0);
+            const bool onr = mine && on_ref(ic);
+            C sq = onr ? xv * xv : C(0);
+            if (mine && ic == kl) *alpha_s = xv;
 #pragma unroll
-                for (int q = 0; q < RPW; ++q) {
-                    const int i = i0 + q;
-                    const C xv = on_ref(i) ? x[q] : C(0);
-                    if (q & 1) s1 += xv * xv; else s0 += xv * xv;
-                    if (i == kl) *alpha_s = x[q];
-                }
-                sig_part[warp] = s0 + s1;
-            }
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            if (c == 0) sig_part[warp] = sq;
             fbar();
-            PROBE(1)
             C sig = C(0);
 #pragma unroll
             for (int w = 0; w < NWF; ++w) sig += sig_part[w];
             C beta, t, scale;
             house(*alpha_s, sig, beta, t, scale);
-            PROBE(2)
-            // the pivot lane forms v for this warp's rows (branch-free selects) and
-            // publishes it through shared memory; the warp reads it back broadcast
-            if (c == kl) {
-#pragma unroll
-                for (int q = 0; q < RPW; ++q) {
-                    const int i = i0 + q;
-                    C vq = x[q] * scale;
-                    vq = on_ref(i) ? vq : C(0);
-                    vq = (i == kl) ? C(1) : vq;
-                    vbuf[q] = vq;
-                    Vs[(i0 + q) * (NB + 1) + kl] = vq;
-                    x[q] = (i == kl) ? beta : (on_ref(i) ? vq : x[q]);
-                }
-                if (warp == 0) tau[J0 + kl] = t;
+            if (mine) {
+                C vq = onr ? xv * scale : C(0);
+                vq = (ic == kl) ? C(1) : vq;
+                vbuf[c] = vq;
+                Vs[ic * (NB + 1) + kl] = vq;
             }
+            if (warp == 0 && c == 0) tau[J0 + kl] = t;
             __syncwarp();
-            PROBE(3)
             C v[RPW];
             C d0 = C(0), d1 = C(0);
 #pragma unroll
             for (int q = 0; q < RPW; ++q) {
+                const int i = i0 + q;
                 v[q] = vbuf[q];
+                if (c == kl) x[q] = (i == kl) ? beta : (on_ref(i) ? v[q] : x[q]);
                 if (q & 1) d1 += v[q] * x[q]; else d0 += v[q] * x[q];
             }
             dpart[warp * 32 + c] = d0 + d1;
-            PROBE(4)
             fbar();
-            PROBE(5)
             if (c > kl && c < NB) {
                 C dd = C(0);
 #pragma unroll
@@ -169,9 +158,11 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
                 const C wc = t * dd;
 #pragma unroll
                 for (int q = 0; q < RPW; ++q) x[q] -= wc * v[q];
+                if (c == kl + 1) {                      // the next step's pivot column
+#pragma unroll
+                    for (int q = 0; q < RPW; ++q) vbuf[q] = x[q];
+                }
             }
-            PROBE(6)
-#undef PROBE
             if (st && threadIdx.x == 0) st[J0 + kl] = stamp_now();
         }
 #pragma unroll

@@ -869,13 +869,16 @@ __global__ void __launch_bounds__(kNTP) k_panel_tt(View<S> V, int64_t m, int64_t
             A[c * lda + TS + r] = (r <= c) ? __ldcg(Rb_g + idx) : C(0);
         }
         __syncthreads();
+        unsigned long long *pst = (g_panel_trace && b == 0 && parent == 0) ? g_panel_trace : nullptr;
+        if (pst && tid == 0) pst[200] = blk::stamp_now();
         blk::qr_blocked<C, TS, true, kNTP, !DEFER>(A, lda, tau, A, lda, aux, house, [&](int j0) {
             for (int idx = tid; idx < TS * NB; idx += kNTP) {
                 const int c = j0 + idx / TS, r = idx % TS;
                 Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
             }
             __syncthreads();
-        });
+        }, pst);
+        if (pst && tid == 0) pst[201] = blk::stamp_now();
         if constexpr (DEFER) {
             for (int idx = tid; idx < TS * TS; idx += kNTP) {
                 const int r = idx / TS, i = idx % TS;
@@ -1080,6 +1083,12 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         int64_t cnt_prev = m;
         for (int j = 1; j <= L; ++j) {
             const int64_t pairs = cnt_prev / 2;
+            unsigned long long *qtrace = nullptr;
+            if (tl_side && j == 1 && pairs > 0) {
+                cudaMalloc(&qtrace, 256 * 8);
+                cudaMemsetAsync(qtrace, 0, 256 * 8, st);
+                cudaMemcpyToSymbolAsync(g_panel_trace, &qtrace, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
+            }
             if (pairs > 0) {
                 k_panel_tt<S, C, TS, DEFER><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, j, ws, ws_elems, a_bstride);
                 bsvd_host::count_launch();
@@ -1087,6 +1096,20 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
             }
             cudaEventRecord(lvl[j], st);
             if (tl_side) tlmark("panel tt", st);
+            if (qtrace) {
+                void *null_ptr = nullptr;
+                cudaMemcpyToSymbolAsync(g_panel_trace, &null_ptr, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
+                std::vector<unsigned long long> h(256);
+                cudaMemcpyAsync(h.data(), qtrace, 256 * 8, cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                const unsigned long long t0 = h[200];
+                fprintf(stderr, "[tt node] col steps (us):");
+                for (int c = 0; c < 128; c += 8) fprintf(stderr, " %d:%.1f", c, (h[c] - t0) * 1e-3);
+                fprintf(stderr, "\n[tt node] subpanel end/T/update (us):");
+                for (int q = 0; q < 12; ++q) fprintf(stderr, " %.1f", (h[128 + q] - t0) * 1e-3);
+                fprintf(stderr, " | total %.1f raw %llu %llu %llu %llu\n", (h[201] - t0) * 1e-3, h[0], h[200], h[128], h[201]);
+                cudaFree(qtrace);
+            }
             if (trail && pairs > 0) {
                 if ((e = level_tu(j, tree_offset(m, j), pairs, true)) != cudaSuccess) return e;
                 if ((e = apply_level(lq, top, k, m, j)) != cudaSuccess) return e;
