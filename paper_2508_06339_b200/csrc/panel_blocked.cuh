@@ -87,7 +87,7 @@ __host__ __device__ constexpr int aux_elems() {
 // sum reductions, reflector scalars) shrink with the warp count, and only
 // the pivot lane forms v (broadcast by shuffle) -- the step is issue-bound.
 template <typename C, int TS, bool TT, int NB, int J0, int NT, typename HS>
-__device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, HS house,
+__device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C *gsub, HS house,
                                          unsigned long long *st) {
     constexpr int R = TT ? (2 * NB + J0) : (TS - J0);    // rows in the sub-panel's row list
     constexpr int NWF = 8;   // measured: 8 warps beat 4 (latency) and 16 (issue)
@@ -107,33 +107,37 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
         C *sig_part = red, *alpha_s = red + NWF, *dpart = red + NWF + 2;
         C *vbuf = dpart + NWF * 32 + i0;
         static_assert(RPW <= 32, "one lane per row of the warp's slab");
-        if (c == 0) {
+        // The pivot lane of step kl (lane kl) publishes its column (vbuf), its
+        // slab's partial norm (sig_part) and alpha right after its own update in
+        // step kl-1, so a step needs two barriers and no separate norm phase.
+        auto publish = [&](int kp) {                    // executed by lane kp
+            C s0 = C(0), s1 = C(0);
 #pragma unroll
-            for (int q = 0; q < RPW; ++q) vbuf[q] = x[q];
-        }
+            for (int q = 0; q < RPW; ++q) {
+                const int i = i0 + q;
+                const bool on = TT ? (i >= NB && i - NB <= J0 + kp) : (i > kp);
+                const C xv = on ? x[q] : C(0);
+                if (q & 1) s1 += xv * xv; else s0 += xv * xv;
+                if (i == kp) *alpha_s = x[q];
+                vbuf[q] = x[q];
+            }
+            sig_part[warp] = s0 + s1;
+        };
+        if (c == 0) publish(0);
         for (int kl = 0; kl < NB; ++kl) {
             // row-list index i is on reflector kl (excluding its unit row kl)?
             auto on_ref = [&](int i) { return TT ? (i >= NB && i - NB <= J0 + kl) : (i > kl); };
-            __syncwarp();
-            // lane q < RPW owns row i0 + q of the pivot column (published by lane kl):
-            // the norm and v are formed lane-parallel instead of by the pivot lane alone
-            const int ic = i0 + c;
-            const bool mine = c < RPW;
-            const C xv = mine ? vbuf[c] : C(0);
-            const bool onr = mine && on_ref(ic);
-            C sq = onr ? xv * xv : C(0);
-            if (mine && ic == kl) *alpha_s = xv;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            if (c == 0) sig_part[warp] = sq;
             fbar();
             C sig = C(0);
 #pragma unroll
             for (int w = 0; w < NWF; ++w) sig += sig_part[w];
             C beta, t, scale;
             house(*alpha_s, sig, beta, t, scale);
-            if (mine) {
-                C vq = onr ? xv * scale : C(0);
+            // v for this warp's rows, lane-parallel (lane q < RPW owns row i0 + q)
+            const int ic = i0 + c;
+            if (c < RPW) {
+                const C xv = vbuf[c];
+                C vq = on_ref(ic) ? xv * scale : C(0);
                 vq = (ic == kl) ? C(1) : vq;
                 vbuf[c] = vq;
                 Vs[ic * (NB + 1) + kl] = vq;
@@ -151,6 +155,14 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
             }
             dpart[warp * 32 + c] = d0 + d1;
             fbar();
+            // lanes c < kl hold v_c (zero off its support) exactly where v_kl lives,
+            // so their dots are G(c, kl) = v_c^T v_kl: T_sub's Gram matrix for free
+            if (warp == 0 && c < kl) {
+                C g = C(0);
+#pragma unroll
+                for (int w = 0; w < NWF; ++w) g += dpart[w * 32 + c];
+                gsub[kl * (NB + 1) + c] = g;
+            }
             if (c > kl && c < NB) {
                 C dd = C(0);
 #pragma unroll
@@ -158,10 +170,7 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, H
                 const C wc = t * dd;
 #pragma unroll
                 for (int q = 0; q < RPW; ++q) x[q] -= wc * v[q];
-                if (c == kl + 1) {                      // the next step's pivot column
-#pragma unroll
-                    for (int q = 0; q < RPW; ++q) vbuf[q] = x[q];
-                }
+                if (c == kl + 1) publish(kl + 1);       // the next step's pivot column
             }
             if (st && threadIdx.x == 0) st[J0 + kl] = stamp_now();
         }
@@ -185,15 +194,10 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
         auto stamp = [&](int id) {
             if (st && threadIdx.x == 0) st[128 + id] = stamp_now();
         };
-        subpanel<C, TS, TT, NB, J0, NT>(A, lda, tau, red, Vs, house, st);
+        subpanel<C, TS, TT, NB, J0, NT>(A, lda, tau, red, Vs, tsub, house, st);   // + G into tsub
         stamp(4 * (J0 / NB) + 0);
         save_r(J0);
-        // ---- T_sub = merge(Vs^T Vs)
-        sgemm<C, 2, 2, NT>(NB, NB, R,
-            [&](int a, int i) { return Vs[i * VLD + a]; },
-            [&](int i, int b) { return Vs[i * VLD + b]; },
-            [&](int a, int b, C v) { if (a < b) tsub[b * LDS + a] = v; });
-        __syncthreads();
+        // ---- T_sub = merge(G): the strictly upper G = Vs^T Vs came out of the factorisation
         panel::build_T_rec<C, NB, NT>(tau + J0, gbuf, [&](int i, int j) -> C & { return tsub[j * LDS + i]; });
         // ---- T[0:J0, J0:J0+NB] = -T[0:J0,0:J0] (Vprev^T Vs) T_sub
         // (FULL_T = false: only the diagonal blocks, which the factorisation

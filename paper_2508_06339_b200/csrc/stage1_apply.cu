@@ -137,11 +137,35 @@ struct View {
 };
 
 // X tile (TS rows from view row r0, BN columns from view column c0, columns
-// >= cmax masked) -> Xs[r][c] (row stride bnp).
+// >= cmax masked) -> Xs[r][c] (row stride bnp).  fp32 full tiles: 16-byte
+// loads -- along the contiguous dimension of either view (column-major RQ
+// side: 8 rows of one column per thread, a full 32-byte sector; LQ side: 4
+// columns of one row).
 template <typename S, typename C, int TS, int BN>
 __device__ __forceinline__ void load_x(const View<S> &V, int64_t r0, int64_t c0, int64_t cmax,
                                        C *Xs, int bnp) {
     using CV = Conv<S, C>;
+    if constexpr (sizeof(S) == 4 && sizeof(C) == 4 && TS % 8 == 0 && BN % 4 == 0) {
+        if (c0 + BN <= cmax) {
+            if (V.rs == 1) {
+                for (int idx = threadIdx.x; idx < (TS / 8) * BN; idx += kNT) {
+                    const int c = idx % BN, u = idx / BN;
+                    const float4 *p = reinterpret_cast<const float4 *>(V.ptr(r0 + 8 * u, c0 + c));
+                    const float4 a = __ldcg(p), b = __ldcg(p + 1);
+                    float *d = Xs + (8 * u) * bnp + c;
+                    d[0] = a.x; d[bnp] = a.y; d[2 * bnp] = a.z; d[3 * bnp] = a.w;
+                    d[4 * bnp] = b.x; d[5 * bnp] = b.y; d[6 * bnp] = b.z; d[7 * bnp] = b.w;
+                }
+            } else {
+                for (int idx = threadIdx.x; idx < TS * (BN / 4); idx += kNT) {
+                    const int c4 = idx % (BN / 4), r = idx / (BN / 4);
+                    const float4 a = __ldcg(reinterpret_cast<const float4 *>(V.ptr(r0 + r, c0 + 4 * c4)));
+                    *reinterpret_cast<float4 *>(Xs + r * bnp + 4 * c4) = a;
+                }
+            }
+            return;
+        }
+    }
     for (int idx = threadIdx.x; idx < TS * BN; idx += kNT) {
         int r, c;
         if (V.rs == 1) { r = idx % TS; c = idx / TS; } else { c = idx % BN; r = idx / BN; }
@@ -149,11 +173,32 @@ __device__ __forceinline__ void load_x(const View<S> &V, int64_t r0, int64_t c0,
     }
 }
 
-// Store the thread's microtile straight from registers.
+// Store the thread's microtile straight from registers (fp32 full tiles:
+// 16-byte stores along the contiguous dimension of the view).
 template <typename S, typename C, typename G>
 __device__ __forceinline__ void store_acc(const View<S> &V, int64_t r0, int64_t c0, int64_t cmax,
                                           const C (&acc)[G::MR][G::NR], const Lane<G> &ln) {
     using CV = Conv<S, C>;
+    if constexpr (sizeof(S) == 4 && sizeof(C) == 4 && G::MR % 4 == 0 && G::NR % 4 == 0) {
+        if (c0 + G::BN <= cmax) {
+            if (V.rs == 1) {
+#pragma unroll
+                for (int j = 0; j < G::NR; ++j)
+#pragma unroll
+                    for (int i = 0; i < G::MR; i += 4)
+                        __stcg(reinterpret_cast<float4 *>(V.ptr(r0 + ln.m0 + i, c0 + ln.n0 + j)),
+                               make_float4(acc[i][j], acc[i + 1][j], acc[i + 2][j], acc[i + 3][j]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+                    for (int j = 0; j < G::NR; j += 4)
+                        __stcg(reinterpret_cast<float4 *>(V.ptr(r0 + ln.m0 + i, c0 + ln.n0 + j)),
+                               make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]));
+            }
+            return;
+        }
+    }
 #pragma unroll
     for (int i = 0; i < G::MR; ++i)
 #pragma unroll
