@@ -827,6 +827,203 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
 }
 }  // namespace ch2
 
+// ---------------------------------------------------------------------------
+// Batched narrow-band chase (b <= 64, many matrices): one CTA per matrix runs
+// its sweeps back to back with the carried-block scheme of ch2 inside the CTA
+// -- the carried block, the new block and the prefetch of the next block all
+// sit in registers (BK x BK tiles, thread (w, l) holds rows l + 32a and
+// columns w + NW q), the pivot passes through shared memory, and because the
+// previous sweep is complete, the next block's load is issued one op ahead.
+namespace ch3 {
+template <typename T, int BK, int NW>
+struct Tile {
+    static constexpr int RA = BK / 32, CQ = BK / NW;
+    T v[RA][CQ];
+};
+
+template <typename T, int BK, int NW>
+__device__ __forceinline__ void load_t(const ch2::BandT<T> &A, const ch2::Blk &g, Tile<T, BK, NW> &x) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < Tile<T, BK, NW>::CQ; ++q) {
+        const int c = w + NW * q;
+#pragma unroll
+        for (int a = 0; a < Tile<T, BK, NW>::RA; ++a) {
+            const int r = l + 32 * a;
+            x.v[a][q] = (r < g.nr && c < g.nc) ? __ldcg(A.at(g.R0 + r, g.C0 + c)) : T(0);
+        }
+    }
+}
+template <typename T, int BK, int NW>
+__device__ __forceinline__ void store_t(const ch2::BandT<T> &A, const ch2::Blk &g, const Tile<T, BK, NW> &x) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < Tile<T, BK, NW>::CQ; ++q) {
+        const int c = w + NW * q;
+#pragma unroll
+        for (int a = 0; a < Tile<T, BK, NW>::RA; ++a) {
+            const int r = l + 32 * a;
+            if (r < g.nr && c < g.nc) __stcg(A.at(g.R0 + r, g.C0 + c), x.v[a][q]);
+        }
+    }
+}
+template <typename T>
+__device__ __forceinline__ void refl(const T *p, int L, T &tau, T &scale, T &beta) {
+    const int lane = threadIdx.x & 31;
+    T sg = T(0);
+    for (int j = 1 + lane; j < L; j += 32) sg = fma(p[j], p[j], sg);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
+    const T alpha = p[0];
+    tau = T(0);
+    scale = T(0);
+    beta = alpha;
+    if (sg != T(0)) {
+        const T nrm = sqrt(fma(alpha, alpha, sg));
+        beta = -copysign(nrm, alpha);
+        tau = (beta - alpha) / beta;
+        scale = T(1) / (alpha - beta);
+    }
+}
+// Left reflector (block rows) on every column; carrier: column 0 is the pivot.
+template <typename T, int BK, int NW>
+__device__ __forceinline__ void left_t(Tile<T, BK, NW> &x, const T *p, int L, T tau, T scale, T beta,
+                                       bool carrier) {
+    constexpr int RA = Tile<T, BK, NW>::RA, CQ = Tile<T, BK, NW>::CQ;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (tau != T(0)) {
+        T va[RA], part[CQ];
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            const int j = l + 32 * a;
+            va[a] = j == 0 ? T(1) : (j < L ? p[j] * scale : T(0));
+        }
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) {
+            T t = va[0] * x.v[0][q];
+#pragma unroll
+            for (int a = 1; a < RA; ++a) t = fma(va[a], x.v[a][q], t);
+            part[q] = t;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int q = 0; q < CQ; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) {
+            const T tw = tau * part[q];
+#pragma unroll
+            for (int a = 0; a < RA; ++a) x.v[a][q] = fma(-tw, va[a], x.v[a][q]);
+        }
+    }
+    if (carrier && w == 0) {
+#pragma unroll
+        for (int a = 0; a < RA; ++a) x.v[a][0] = (l + 32 * a == 0) ? beta : T(0);
+    }
+}
+// Right reflector (block columns) on every row (dots over the NW warps
+// through shared memory red[NW][BK]); carrier: row 0 is the pivot.
+template <typename T, int BK, int NW>
+__device__ __forceinline__ void right_t(Tile<T, BK, NW> &x, const T *p, int L, T tau, T scale, T beta,
+                                        bool carrier, T *red) {
+    constexpr int RA = Tile<T, BK, NW>::RA, CQ = Tile<T, BK, NW>::CQ;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (tau != T(0)) {                     // uniform across the CTA
+        T vq[CQ];
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) {
+            const int c = w + NW * q;
+            vq[q] = c == 0 ? T(1) : (c < L ? p[c] * scale : T(0));
+        }
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            T t = x.v[a][0] * vq[0];
+#pragma unroll
+            for (int q = 1; q < CQ; ++q) t = fma(x.v[a][q], vq[q], t);
+            red[w * BK + l + 32 * a] = t;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            const int r = l + 32 * a;
+            T d = T(0);
+#pragma unroll
+            for (int g = 0; g < NW; ++g) d += red[g * BK + r];
+            const T td = tau * d;
+#pragma unroll
+            for (int q = 0; q < CQ; ++q) x.v[a][q] = fma(-td, vq[q], x.v[a][q]);
+        }
+        __syncthreads();                   // red is reused by the next right op
+    }
+    if (carrier && l == 0) {
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) x.v[0][q] = (w + NW * q == 0) ? beta : T(0);
+    }
+}
+
+template <typename T, int BK, int NW>
+__global__ void __launch_bounds__(NW * 32) k_chase_cta(T *band, int64_t n, int b, int64_t ld,
+                                                      int64_t batch) {
+    using TL = Tile<T, BK, NW>;
+    constexpr int RA = TL::RA, CQ = TL::CQ;
+    __shared__ T piv[BK];
+    __shared__ T red[NW * BK];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int64_t m = blockIdx.x; m < batch; m += gridDim.x) {
+        const ch2::BandT<T> A{band + m * n * ld, n, ld, b};
+        for (int64_t s = 0; s + 2 < n; ++s) {
+            const int nops = chase_nops(s, n, b);
+            TL xc, xn, xp;
+            __syncthreads();               // the previous sweep's stores are visible
+            ch2::Blk g = ch2::geom(s, 0, n, b), gc = g;
+            load_t<T, BK, NW>(A, g, xn);
+            int L = (int)min((int64_t)b, n - s - 1);
+            for (int j = threadIdx.x; j < BK; j += NW * 32) piv[j] = j < L ? __ldcg(A.at(s, s + 1 + j)) : T(0);
+            __syncthreads();
+            for (int k = 0; k < nops; ++k) {
+                const ch2::Blk gn = k + 1 < nops ? ch2::geom(s, k + 1, n, b) : g;
+                if (k + 1 < nops) load_t<T, BK, NW>(A, gn, xp);      // prefetch block k+1
+                T tau, scale, beta;
+                refl<T>(piv, L, tau, scale, beta);
+                if (k == 0 && threadIdx.x == 0) __stcg(A.at(s, s + 1), beta);
+                if (k & 1) {
+                    left_t<T, BK, NW>(xn, piv, L, tau, scale, beta, false);
+                    left_t<T, BK, NW>(xc, piv, L, tau, scale, beta, true);
+                } else {
+                    right_t<T, BK, NW>(xn, piv, L, tau, scale, beta, false, red);
+                    if (k > 0) right_t<T, BK, NW>(xc, piv, L, tau, scale, beta, true, red);
+                }
+                if (k > 0) store_t<T, BK, NW>(A, gc, xc);               // block k-1 is final
+                __syncthreads();                                        // piv fully consumed
+                if (k + 1 < nops) {
+                    // op k+1's pivot: column 0 (left op next) or row 0 (right op next) of block k
+                    if (!(k & 1)) {
+                        if (w == 0) {
+#pragma unroll
+                            for (int a = 0; a < RA; ++a) piv[l + 32 * a] = xn.v[a][0];
+                        }
+                        L = g.nr;
+                    } else {
+                        if (l == 0) {
+#pragma unroll
+                            for (int q = 0; q < CQ; ++q) piv[w + NW * q] = xn.v[0][q];
+                        }
+                        L = g.nc;
+                    }
+                    __syncthreads();
+                    xc = xn;
+                    xn = xp;
+                    gc = g;
+                    g = gn;
+                } else {
+                    store_t<T, BK, NW>(A, g, xn);                        // the sweep's last block
+                }
+            }
+        }
+    }
+}
+}  // namespace ch3
+
 // ops (= blocks) of sweep 0, the longest sweep: the per-sweep flag stride of
 // the carried-block chase
 static int chase_max_ops(int64_t n, int b) { return 3 + (int)(2 * ((n + b - 1) / b)); }
@@ -927,6 +1124,41 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
             bsvd_host::count_launch();
             if ((err = cudaGetLastError()) != cudaSuccess) return err;
             if ((err = launch_chase2<double>((double *)bandp, n, b, ld, batch, progress, st)) != cudaSuccess) return err;
+            k_extract_bidiag<double><<<g2, 256, 0, st>>>((const double *)bandp, n, ld, b, d, e);
+        }
+        bsvd_host::count_launch();
+        return cudaGetLastError();
+    }
+    if (n > 2 && b <= 64 && batch >= 512 && !getenv("BSVD_CHASE_PIPELINED") && !getenv("BSVD_CHASE_SEQ")) {
+        // many matrices, narrow band: one CTA per matrix (ch3), compute precision
+        const bool f32 = sizeof(S) < 8 && !getenv("BSVD_CHASE_F64");
+        const size_t es = f32 ? sizeof(float) : sizeof(double);
+        char *bandp = (char *)ws;
+        cudaError_t err = cudaMemsetAsync(bandp, 0, (size_t)batch * n * ld * es, st);
+        if (err != cudaSuccess) return err;
+        const int64_t total = n * (int64_t)(bw + 1);
+        dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 4096), (unsigned)batch);
+        dim3 g2((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch);
+        int dev = 0, nsm = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (f32) {
+            k_pack_band<S, float><<<grid, 256, 0, st>>>(a, n, lda, a_bstride, bw, (float *)bandp, ld, b);
+            bsvd_host::count_launch();
+            auto kern = ch3::k_chase_cta<float, 64, 8>;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+            kern<<<(unsigned)std::min<int64_t>(batch, (int64_t)nsm * std::max(per_sm, 1)), 256, 0, st>>>(
+                (float *)bandp, n, b, ld, batch);
+            bsvd_host::count_launch();
+            k_extract_bidiag<float><<<g2, 256, 0, st>>>((const float *)bandp, n, ld, b, d, e);
+        } else {
+            k_pack_band<S, double><<<grid, 256, 0, st>>>(a, n, lda, a_bstride, bw, (double *)bandp, ld, b);
+            bsvd_host::count_launch();
+            auto kern = ch3::k_chase_cta<double, 64, 8>;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+            kern<<<(unsigned)std::min<int64_t>(batch, (int64_t)nsm * std::max(per_sm, 1)), 256, 0, st>>>(
+                (double *)bandp, n, b, ld, batch);
+            bsvd_host::count_launch();
             k_extract_bidiag<double><<<g2, 256, 0, st>>>((const double *)bandp, n, ld, b, d, e);
         }
         bsvd_host::count_launch();
