@@ -238,7 +238,7 @@ using namespace apply;
 
 // Leaf level: grid (column blocks, m tile rows, batch).
 template <typename S, typename C, int TS>
-__global__ void __launch_bounds__(apply::kNT) k_apply_leaf(View<S> V, int64_t top, int64_t cbase,
+__global__ void __launch_bounds__(apply::kNT, 3) k_apply_leaf(View<S> V, int64_t top, int64_t cbase,
                                                            int64_t ncols, const C *nodes,
                                                            int64_t ts2x3, int64_t ws_bstride,
                                                            int64_t a_bstride) {
@@ -247,8 +247,7 @@ __global__ void __launch_bounds__(apply::kNT) k_apply_leaf(View<S> V, int64_t to
     constexpr int KC = (G::KC < TS) ? G::KC : TS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *Abuf = (C *)smem_raw;
-    C *Xs = Abuf + 2 * KC * TS;
-    C *Ws = Xs + TS * BNP;
+    C *Xs = Abuf + 2 * KC * TS;                  // X, then W (one tile: 3 CTAs/SM)
     const int64_t b = blockIdx.z, l = blockIdx.y;
     V.base += b * a_bstride;
     nodes += b * ws_bstride;
@@ -260,11 +259,17 @@ __global__ void __launch_bounds__(apply::kNT) k_apply_leaf(View<S> V, int64_t to
     __syncthreads();
     C acc[G::MR][G::NR];
     zero<C, G>(acc);
-    gemm<C, TS, G, false, BNP, 2>(Vk, Xs, Abuf, acc, ln);   // W = V^T X
-    to_smem<C, G>(acc, Ws, BNP, ln);
-    init_from<C, G>(acc, Xs, BNP, ln);
+    gemm<C, TS, G, false, BNP, 2>(Vk, Xs, Abuf, acc, ln);   // W = V^T X (ends on a barrier)
+    C xr[G::MR][G::NR];
+    init_from<C, G>(xr, Xs, BNP, ln);                       // the thread's X microtile
+    __syncthreads();                                        // every X read before W lands
+    to_smem<C, G>(acc, Xs, BNP, ln);
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int j = 0; j < G::NR; ++j) acc[i][j] = xr[i][j];
     __syncthreads();
-    gemm<C, TS, G, true, BNP>(Um, Ws, Abuf, acc, ln);    // X -= U W
+    gemm<C, TS, G, true, BNP>(Um, Xs, Abuf, acc, ln);       // X -= U W
     store_acc<S, C, G>(V, r0, c0, cmax, acc, ln);
 }
 
@@ -324,7 +329,7 @@ size_t apply_smem(bool tt) {
     using G = Geo<C, TS>;
     constexpr int BNP = G::BN + 16 / (int)sizeof(C);
     constexpr int KC = (G::KC < TS) ? G::KC : TS;
-    return (size_t)(2 * KC * TS + 2 * TS * BNP) * sizeof(C);
+    return (size_t)(2 * KC * TS + (tt ? 2 : 1) * TS * BNP) * sizeof(C);
 }
 
 // Host side: one launch for the leaves, one per tree level.
