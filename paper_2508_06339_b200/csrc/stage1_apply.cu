@@ -36,6 +36,10 @@ template <int TS> struct Geo<float, TS> {
     static constexpr int MR = BM / (WGM * LM);
     static constexpr int NR = BN / (WGN * LN);
     static constexpr int KC = 32;
+    // balanced rows: warp row wm owns the 16-row half-blocks wm and 7 - wm,
+    // so a triangular operand gives every warp the same number of nonzero
+    // K-chunks (each warp's two halves skip independently)
+    static constexpr bool BAL = (TS == 128);
 };
 template <int TS> struct Geo<double, TS> {
     static constexpr int BM = TS;
@@ -47,6 +51,7 @@ template <int TS> struct Geo<double, TS> {
     static constexpr int MR = BM / (WGM * LM);
     static constexpr int NR = BN / (WGN * LN);
     static constexpr int KC = 16;
+    static constexpr bool BAL = false;
 };
 
 template <typename C> struct Vec;
@@ -61,17 +66,27 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Thread's microtile coordinates.
+// Thread's microtile coordinates: rows m0.. (first half of the microtile)
+// and m1.. (second half), columns n0..
 template <typename G>
 struct Lane {
-    int m0, n0;
+    int m0, m1, n0, wm;
     __device__ Lane() {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        const int wm = warp % G::WGM, wn = warp / G::WGM;
+        wm = warp % G::WGM;
+        const int wn = warp / G::WGM;
         const int lm = lane % G::LM, ln = lane / G::LM;
-        m0 = wm * (G::BM / G::WGM) + lm * G::MR;
+        if constexpr (G::BAL) {
+            constexpr int HB = G::BM / (2 * G::WGM);        // half-block rows
+            m0 = wm * HB + lm * (G::MR / 2);
+            m1 = (2 * G::WGM - 1 - wm) * HB + lm * (G::MR / 2);
+        } else {
+            m0 = wm * (G::BM / G::WGM) + lm * G::MR;
+            m1 = m0 + G::MR / 2;
+        }
         n0 = wn * (G::BN / G::WGN) + ln * G::NR;
     }
+    __device__ __forceinline__ int row(int i) const { return i < G::MR / 2 ? m0 + i : m1 + (i - G::MR / 2); }
 };
 
 // acc[i][j] += sign * sum_k A[k][m0+i] * Bs[k][n0+j]; A global [TS][TS] streamed
@@ -107,23 +122,61 @@ __device__ __forceinline__ void gemm(const C *__restrict__ Ag, const C *Bs, C *A
         __syncthreads();
         const C *As = Abuf + (ch & 1) * CH;
         const C *Bk = Bs + (size_t)ch * KC * bnp;
-        constexpr bool SKIP = TRI != 0 && KC == G::BM / G::WGM;
-        const int wm = (threadIdx.x >> 5) % G::WGM;          // the warp's row block
-        const bool zero = SKIP && (TRI == 1 ? ch > wm : ch < wm);
+        constexpr int H = G::MR / 2;
+        bool za = false, zb = false;                      // microtile halves entirely zero
+        if constexpr (TRI != 0 && G::BAL && KC == 2 * (G::BM / (2 * G::WGM))) {
+            const int ha = ln.wm, hb = 2 * G::WGM - 1 - ln.wm;   // half-block indices
+            za = TRI == 1 ? ch > (ha >> 1) : ch < (ha >> 1);
+            zb = TRI == 1 ? ch > (hb >> 1) : ch < (hb >> 1);
+        } else if constexpr (TRI != 0 && !G::BAL && KC == G::BM / G::WGM) {
+            za = zb = TRI == 1 ? ch > ln.wm : ch < ln.wm;
+        }
+        if (!za && !zb) {
 #pragma unroll 4
-        for (int k = 0; k < (zero ? 0 : KC); ++k) {
-            C a[G::MR], b[G::NR];
+            for (int k = 0; k < KC; ++k) {
+                C a[G::MR], b[G::NR];
 #pragma unroll
-            for (int i = 0; i < G::MR; ++i) a[i] = As[k * TS + ln.m0 + i];
+                for (int i = 0; i < H; ++i) a[i] = As[k * TS + ln.m0 + i];
 #pragma unroll
-            for (int j = 0; j < G::NR; ++j) b[j] = Bk[k * bnp + ln.n0 + j];
+                for (int i = 0; i < H; ++i) a[H + i] = As[k * TS + ln.m1 + i];
 #pragma unroll
-            for (int i = 0; i < G::MR; ++i)
+                for (int j = 0; j < G::NR; ++j) b[j] = Bk[k * bnp + ln.n0 + j];
 #pragma unroll
-                for (int j = 0; j < G::NR; ++j) {
-                    if (NEG) acc[i][j] -= a[i] * b[j];
-                    else acc[i][j] += a[i] * b[j];
+                for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+                    for (int j = 0; j < G::NR; ++j) {
+                        if (NEG) acc[i][j] -= a[i] * b[j];
+                        else acc[i][j] += a[i] * b[j];
+                    }
+            }
+        } else if (!za || !zb) {                          // one half only
+            const int mh = za ? ln.m1 : ln.m0, io = za ? H : 0;
+#pragma unroll 4
+            for (int k = 0; k < KC; ++k) {
+                C a[H], b[G::NR];
+#pragma unroll
+                for (int i = 0; i < H; ++i) a[i] = As[k * TS + mh + i];
+#pragma unroll
+                for (int j = 0; j < G::NR; ++j) b[j] = Bk[k * bnp + ln.n0 + j];
+                if (za) {
+#pragma unroll
+                    for (int i = 0; i < H; ++i)
+#pragma unroll
+                        for (int j = 0; j < G::NR; ++j) {
+                            if (NEG) acc[H + i][j] -= a[i] * b[j];
+                            else acc[H + i][j] += a[i] * b[j];
+                        }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < H; ++i)
+#pragma unroll
+                        for (int j = 0; j < G::NR; ++j) {
+                            if (NEG) acc[i][j] -= a[i] * b[j];
+                            else acc[i][j] += a[i] * b[j];
+                        }
                 }
+                (void)io;
+            }
         }
         __syncthreads();   // buffer (ch & 1) is refilled by issue(ch + 2)
     }
@@ -186,14 +239,14 @@ __device__ __forceinline__ void store_acc(const View<S> &V, int64_t r0, int64_t 
                 for (int j = 0; j < G::NR; ++j)
 #pragma unroll
                     for (int i = 0; i < G::MR; i += 4)
-                        __stcg(reinterpret_cast<float4 *>(V.ptr(r0 + ln.m0 + i, c0 + ln.n0 + j)),
+                        __stcg(reinterpret_cast<float4 *>(V.ptr(r0 + ln.row(i), c0 + ln.n0 + j)),
                                make_float4(acc[i][j], acc[i + 1][j], acc[i + 2][j], acc[i + 3][j]));
             } else {
 #pragma unroll
                 for (int i = 0; i < G::MR; ++i)
 #pragma unroll
                     for (int j = 0; j < G::NR; j += 4)
-                        __stcg(reinterpret_cast<float4 *>(V.ptr(r0 + ln.m0 + i, c0 + ln.n0 + j)),
+                        __stcg(reinterpret_cast<float4 *>(V.ptr(r0 + ln.row(i), c0 + ln.n0 + j)),
                                make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]));
             }
             return;
@@ -203,7 +256,7 @@ __device__ __forceinline__ void store_acc(const View<S> &V, int64_t r0, int64_t 
     for (int i = 0; i < G::MR; ++i)
 #pragma unroll
         for (int j = 0; j < G::NR; ++j)
-            if (c0 + ln.n0 + j < cmax) *V.ptr(r0 + ln.m0 + i, c0 + ln.n0 + j) = CV::st(acc[i][j]);
+            if (c0 + ln.n0 + j < cmax) *V.ptr(r0 + ln.row(i), c0 + ln.n0 + j) = CV::st(acc[i][j]);
 }
 
 template <typename C, typename G>
@@ -212,7 +265,7 @@ __device__ __forceinline__ void init_from(C (&acc)[G::MR][G::NR], const C *Xs, i
 #pragma unroll
     for (int i = 0; i < G::MR; ++i)
 #pragma unroll
-        for (int j = 0; j < G::NR; ++j) acc[i][j] = Xs[(ln.m0 + i) * bnp + ln.n0 + j];
+        for (int j = 0; j < G::NR; ++j) acc[i][j] = Xs[ln.row(i) * bnp + ln.n0 + j];
 }
 
 template <typename C, typename G>
@@ -229,7 +282,7 @@ __device__ __forceinline__ void to_smem(const C (&acc)[G::MR][G::NR], C *Ws, int
 #pragma unroll
     for (int i = 0; i < G::MR; ++i)
 #pragma unroll
-        for (int j = 0; j < G::NR; ++j) Ws[(ln.m0 + i) * bnp + ln.n0 + j] = acc[i][j];
+        for (int j = 0; j < G::NR; ++j) Ws[ln.row(i) * bnp + ln.n0 + j] = acc[i][j];
 }
 
 }  // namespace apply
