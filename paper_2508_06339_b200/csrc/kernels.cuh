@@ -48,10 +48,13 @@ template <typename S, typename C, int TS>
 cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
                                 int64_t top, int64_t k, int64_t m, const C *nodes,
                                 int64_t ws_bstride, cudaStream_t st);
+// ext != nullptr: two-tile leaves (m counts them; mtiles = the panel's tile
+// rows), leaf-level update from the leaf2 region, TT tile rows strided by 2.
 template <typename S, typename C, int TS>
 cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
                                int64_t top, int64_t k, int64_t m, const C *nodes,
-                               int64_t ws_bstride, int j, cudaStream_t st);
+                               int64_t ws_bstride, int j, cudaStream_t st, const C *ext = nullptr,
+                               int64_t mtiles = 0);
 // Tensor-core (tcgen05 3xTF32) variant for fp32 compute at ts = 128.
 template <typename S>
 cudaError_t launch_apply_level_tc(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq, int64_t top,

@@ -75,10 +75,11 @@ struct NBsel {   // sub-panel width: 16 keeps fp64 ts=128 leaves inside shared m
 };
 
 // scratch elements needed by qr_blocked (Vs | wbuf | gbuf | tsub | red)
-template <typename C, int TS>
+// ROWS: rows of a LEAF operand (TS for a tile, 2 TS for a two-tile leaf)
+template <typename C, int TS, int ROWS = TS>
 __host__ __device__ constexpr int aux_elems() {
     constexpr int NB = NBsel<C, TS>::v;
-    return (TS + NB) * (NB + 1) + 2 * NB * TS + NB * (NB + 1) + 16 * 34 + 8 + (TS + 2 * NB);
+    return (ROWS + NB) * (NB + 1) + 2 * NB * TS + NB * (NB + 1) + 16 * 34 + 8 + (ROWS + 2 * NB);
 }
 
 // Step 1: register-resident factorisation of sub-panel J0 by the first NWF
@@ -86,10 +87,10 @@ __host__ __device__ constexpr int aux_elems() {
 // Fewer, fatter warps: the per-step overheads that every warp pays (partial-
 // sum reductions, reflector scalars) shrink with the warp count, and only
 // the pivot lane forms v (broadcast by shuffle) -- the step is issue-bound.
-template <typename C, int TS, bool TT, int NB, int J0, int NT, typename HS>
+template <typename C, int TS, bool TT, int NB, int J0, int NT, int ROWS, typename HS>
 __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C *gsub, HS house,
                                          unsigned long long *st) {
-    constexpr int R = TT ? (2 * NB + J0) : (TS - J0);    // rows in the sub-panel's row list
+    constexpr int R = TT ? (2 * NB + J0) : (ROWS - J0);  // rows in the sub-panel's row list
     constexpr int NWF = 8;   // measured: 8 warps beat 4 (latency) and 16 (issue)
     constexpr int RPW = R / NWF;
     static_assert(R % NWF == 0, "row list must split evenly over the factor warps");
@@ -181,20 +182,20 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C
     __syncthreads();
 }
 
-template <typename C, int TS, bool TT, int NB, int J0, int NT, bool FULL_T, typename HS, typename SaveR>
+template <typename C, int TS, bool TT, int NB, int J0, int NT, bool FULL_T, int ROWS, typename HS, typename SaveR>
 __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C *aux, HS house,
                                         SaveR save_r, unsigned long long *st) {
     if constexpr (J0 < TS) {
-        constexpr int R = TT ? (2 * NB + J0) : (TS - J0);
+        constexpr int R = TT ? (2 * NB + J0) : (ROWS - J0);
         constexpr int LDS = NB + 1;
         constexpr int VLD = NB + 1;   // padded: the update reads Vs down its columns
-        C *Vs = aux, *wbuf = Vs + (TS + NB) * VLD, *gbuf = wbuf + NB * TS;
+        C *Vs = aux, *wbuf = Vs + (ROWS + NB) * VLD, *gbuf = wbuf + NB * TS;
         C *tsub = gbuf + NB * TS, *red = tsub + NB * LDS;
         auto row = [](int i) { return TT ? (i < NB ? J0 + i : TS + (i - NB)) : (J0 + i); };
         auto stamp = [&](int id) {
             if (st && threadIdx.x == 0) st[128 + id] = stamp_now();
         };
-        subpanel<C, TS, TT, NB, J0, NT>(A, lda, tau, red, Vs, tsub, house, st);   // + G into tsub
+        subpanel<C, TS, TT, NB, J0, NT, ROWS>(A, lda, tau, red, Vs, tsub, house, st);   // + G into tsub
         stamp(4 * (J0 / NB) + 0);
         save_r(J0);
         // ---- T_sub = merge(G): the strictly upper G = Vs^T Vs came out of the factorisation
@@ -246,14 +247,14 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
             __syncthreads();
         }
         stamp(4 * (J0 / NB) + 2);
-        qr_step<C, TS, TT, NB, J0 + NB, NT, FULL_T>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
+        qr_step<C, TS, TT, NB, J0 + NB, NT, FULL_T, ROWS>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
     }
 }
 
-template <typename C, int TS, bool TT, int NT, bool FULL_T = true, typename HS, typename SaveR>
+template <typename C, int TS, bool TT, int NT, bool FULL_T = true, int ROWS = TS, typename HS, typename SaveR>
 __device__ void qr_blocked(C *A, int lda, C *tau, C *Tm, int ldt, C *aux, HS house, SaveR save_r,
                            unsigned long long *st = nullptr) {
-    qr_step<C, TS, TT, NBsel<C, TS>::v, 0, NT, FULL_T>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
+    qr_step<C, TS, TT, NBsel<C, TS>::v, 0, NT, FULL_T, ROWS>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
 }
 
 }  // namespace blk

@@ -333,7 +333,8 @@ template <typename S, typename C, int TS>
 __global__ void __launch_bounds__(apply::kNT) k_apply_tt(View<S> V, int64_t top, int64_t cbase,
                                                          int64_t ncols, const C *nodes,
                                                          int64_t ts2x3, int64_t slot0, int j,
-                                                         int64_t ws_bstride, int64_t a_bstride) {
+                                                         int64_t ws_bstride, int64_t a_bstride,
+                                                         int lstride) {
     using G = Geo<C, TS>;
     constexpr int BNP = G::BN + 16 / (int)sizeof(C);
     constexpr int KC = (G::KC < TS) ? G::KC : TS;
@@ -346,8 +347,8 @@ __global__ void __launch_bounds__(apply::kNT) k_apply_tt(View<S> V, int64_t top,
     nodes += b * ws_bstride;
     const C *Vk = nodes + (slot0 + p) * ts2x3, *Um = Vk + (int64_t)TS * TS, *Tt = Um + (int64_t)TS * TS;
     const int64_t c0 = cbase + (int64_t)blockIdx.x * G::BN, cmax = cbase + ncols;
-    const int64_t rt = (top + ((2 * p) << (j - 1))) * TS;
-    const int64_t rb = (top + ((2 * p + 1) << (j - 1))) * TS;
+    const int64_t rt = (top + lstride * ((2 * p) << (j - 1))) * TS;
+    const int64_t rb = (top + lstride * ((2 * p + 1) << (j - 1))) * TS;
     const Lane<G> ln;
     load_x<S, C, TS, G::BN>(V, rt, c0, cmax, Xt, BNP);
     load_x<S, C, TS, G::BN>(V, rb, c0, cmax, Xb, BNP);
@@ -375,6 +376,59 @@ __global__ void __launch_bounds__(apply::kNT) k_apply_tt(View<S> V, int64_t top,
     init_from<C, G>(acc, Xb, BNP, ln);
     gemm<C, TS, G, true, BNP, 2>(Um, Xt, Abuf, acc, ln);    // X_bot -= Vb W2 (Um = Vb^T layout)
     store_acc<S, C, G>(V, rb, c0, cmax, acc, ln);
+}
+
+// Two-tile leaves (stage1_tree.cu k_panel_leaf2): grid (column blocks,
+// super-leaves, batch).  V = [V1; V2] (V1 unit lower, V2 dense), U = [U1; U2]:
+//   W = V1^T X1 + V2^T X2 ;  X1 -= U1 W ;  X2 -= U2 W
+// (the second tile absent past the panel's end).  X1's tile carries W once
+// X1's microtile is in registers: two shared tiles, 2 CTAs/SM.
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(apply::kNT, 2) k_apply_leaf2(View<S> V, int64_t top, int64_t m,
+                                                              int64_t cbase, int64_t ncols, const C *nodes,
+                                                              const C *ext, int64_t ts2x3,
+                                                              int64_t ws_bstride, int64_t a_bstride) {
+    using G = Geo<C, TS>;
+    constexpr int BNP = G::BN + 16 / (int)sizeof(C);
+    constexpr int KC = (G::KC < TS) ? G::KC : TS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *Abuf = (C *)smem_raw;
+    C *X1 = Abuf + 2 * KC * TS;
+    C *X2 = X1 + TS * BNP;
+    const int64_t b = blockIdx.z, l = blockIdx.y;
+    const int64_t ts2 = (int64_t)TS * TS;
+    V.base += b * a_bstride;
+    nodes += b * ws_bstride;
+    ext += b * ws_bstride;
+    const C *Vk = nodes + l * ts2x3, *Um = Vk + ts2;
+    const C *V2 = ext + l * 2 * ts2, *U2 = V2 + ts2;
+    const int64_t c0 = cbase + (int64_t)blockIdx.x * G::BN, cmax = cbase + ncols;
+    const int64_t r1 = (top + 2 * l) * TS, r2 = r1 + TS;
+    const bool two = 2 * l + 1 < m;
+    const Lane<G> ln;
+    load_x<S, C, TS, G::BN>(V, r1, c0, cmax, X1, BNP);
+    if (two) load_x<S, C, TS, G::BN>(V, r2, c0, cmax, X2, BNP);
+    __syncthreads();
+    C acc[G::MR][G::NR];
+    zero<C, G>(acc);
+    gemm<C, TS, G, false, BNP, 2>(Vk, X1, Abuf, acc, ln);      // V1^T X1 (V1 unit lower)
+    if (two) gemm<C, TS, G, false, BNP>(V2, X2, Abuf, acc, ln);   // + V2^T X2
+    C xr[G::MR][G::NR];
+    init_from<C, G>(xr, X1, BNP, ln);
+    __syncthreads();
+    to_smem<C, G>(acc, X1, BNP, ln);                           // W
+#pragma unroll
+    for (int i = 0; i < G::MR; ++i)
+#pragma unroll
+        for (int jx = 0; jx < G::NR; ++jx) acc[i][jx] = xr[i][jx];
+    __syncthreads();
+    gemm<C, TS, G, true, BNP>(Um, X1, Abuf, acc, ln);          // X1 -= U1 W
+    store_acc<S, C, G>(V, r1, c0, cmax, acc, ln);
+    if (two) {
+        init_from<C, G>(acc, X2, BNP, ln);
+        gemm<C, TS, G, true, BNP>(U2, X1, Abuf, acc, ln);      // X2 -= U2 W
+        store_acc<S, C, G>(V, r2, c0, cmax, acc, ln);
+    }
 }
 
 template <typename C, int TS>
@@ -420,7 +474,7 @@ cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstrid
         const int64_t pairs = cnt_prev / 2;                // nodes with a right child
         if (pairs > 0) {
             k_apply_tt<S, C, TS><<<dim3(gx, (unsigned)pairs, (unsigned)batch), apply::kNT, stt, st>>>(
-                V, top, cbase, ncols, nodes, ts2x3, off, j, ws_bstride, a_bstride);
+                V, top, cbase, ncols, nodes, ts2x3, off, j, ws_bstride, a_bstride, 1);
             bsvd_host::count_launch();
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
@@ -435,7 +489,8 @@ cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstrid
 template <typename S, typename C, int TS>
 cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,
                                int64_t top, int64_t k, int64_t m, const C *nodes,
-                               int64_t ws_bstride, int j, cudaStream_t st) {
+                               int64_t ws_bstride, int j, cudaStream_t st, const C *ext,
+                               int64_t mtiles) {
     using G = Geo<C, TS>;
     const int64_t ncols = (n / TS - 1 - k) * TS;
     if (ncols <= 0) return cudaSuccess;
@@ -446,6 +501,19 @@ cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride
     static size_t set_leaf = 0, set_tt = 0;
     const size_t sl = apply_smem<C, TS>(false), stt = apply_smem<C, TS>(true);
     cudaError_t e;
+    const int lstride = ext ? 2 : 1;                    // m counts two-tile leaves
+    if (j == 0 && ext) {
+        static size_t set2 = 0;
+        const size_t s2 = apply_smem<C, TS>(true);
+        if (s2 > set2) {
+            if ((e = cudaFuncSetAttribute(k_apply_leaf2<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)) != cudaSuccess) return e;
+            set2 = s2;
+        }
+        k_apply_leaf2<S, C, TS><<<dim3(gx, (unsigned)m, (unsigned)batch), apply::kNT, s2, st>>>(
+            V, top, mtiles, cbase, ncols, nodes, ext, ts2x3, ws_bstride, a_bstride);
+        bsvd_host::count_launch();
+        return cudaGetLastError();
+    }
     if (j == 0) {
         if (sl > set_leaf) {
             if ((e = cudaFuncSetAttribute(k_apply_leaf<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sl)) != cudaSuccess) return e;
@@ -469,7 +537,7 @@ cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride
     const int64_t pairs = cnt_prev / 2;
     if (pairs <= 0) return cudaSuccess;
     k_apply_tt<S, C, TS><<<dim3(gx, (unsigned)pairs, (unsigned)batch), apply::kNT, stt, st>>>(
-        V, top, cbase, ncols, nodes, ts2x3, off, j, ws_bstride, a_bstride);
+        V, top, cbase, ncols, nodes, ts2x3, off, j, ws_bstride, a_bstride, lstride);
     bsvd_host::count_launch();
     return cudaGetLastError();
 }
@@ -480,7 +548,8 @@ cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride
                                                        int64_t, cudaStream_t);                  \
     template cudaError_t launch_apply_level<S, C, TS>(S *, int64_t, int64_t, int64_t, bool,     \
                                                       int64_t, int64_t, int64_t, const C *,     \
-                                                      int64_t, int, cudaStream_t);
+                                                      int64_t, int, cudaStream_t, const C *,    \
+                                                      int64_t);
 #define INST3(TS) INST(double, double, TS) INST(float, float, TS) INST(__half, float, TS)
 INST3(16)
 INST3(32)

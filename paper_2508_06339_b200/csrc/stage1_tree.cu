@@ -95,12 +95,19 @@ __host__ __device__ inline size_t tree_img_offset(int64_t N, int ts) {
     return (e + 63) & ~(size_t)63;
 }
 
+// Elements before the two-tile-leaf region (per super-leaf: V and U rows
+// ts..2ts-1, ts^2 each; the first ts rows stay in the leaf's Vk / Um slots).
+template <typename C>
+__host__ __device__ inline size_t tree_leaf2_offset(int64_t N, int ts) {
+    size_t e = tree_img_offset<C>(N, ts);
+    if (tree_tc<C>(ts)) e += (size_t)tree_slots(N) * 6 * ts * ts;   // hi/lo images, 3 per node
+    return (e + 63) & ~(size_t)63;
+}
 template <typename C>
 __host__ __device__ inline size_t tree_ws_elems(int64_t N, int ts) {
     // rounded to 64 elements: every batch member's slice stays 256-byte
     // aligned for the 16-byte cp.async / bulk-copy tile loads
-    size_t e = tree_img_offset<C>(N, ts);
-    if (tree_tc<C>(ts)) e += (size_t)tree_slots(N) * 6 * ts * ts;   // hi/lo images, 3 per node
+    const size_t e = tree_leaf2_offset<C>(N, ts) + (size_t)N * 2 * ts * ts;
     return (e + 63) & ~(size_t)63;
 }
 
@@ -836,6 +843,114 @@ __global__ void __launch_bounds__(kNTP) k_panel_leaf(View<S> V, int64_t m, int64
     }
 }
 
+// Two-tile leaves (fp32 compute, ts = 128): super-leaf l factors the dense
+// 2ts x ts panel of tile rows top+2l and top+2l+1 (the second a zero tile
+// past the panel's end) in one blocked QR -- the leaf level and the first
+// TT level of the single-tile tree in one node.  V rows 0..ts-1 go to the
+// leaf's Vk slot, rows ts..2ts-1 to the leaf2 region; tau into Tt.
+template <typename C, int TS>
+struct Leaf2 {
+    static constexpr int LD = 2 * TS + 1;
+    static constexpr int AUX = blk::aux_elems<C, TS, 2 * TS>();
+    static constexpr size_t smem = (size_t)(TS * LD + AUX + TS + 8) * sizeof(C);
+    static constexpr bool ok = sizeof(C) == 4 && TS == 128 && smem <= 227 * 1024;
+};
+
+template <typename S, typename C, int TS>
+__global__ void __launch_bounds__(kNTP) k_panel_leaf2(View<S> V, int64_t m, int64_t m2, int64_t top,
+                                                     int64_t k, TreeWs<C> ws, C *ext,
+                                                     int64_t ws_bstride, int64_t a_bstride) {
+    using CV = Conv<S, C>;
+    using L2 = Leaf2<C, TS>;
+    constexpr int NB = blk::NBsel<C, TS>::v;
+    constexpr int lda = L2::LD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *A = (C *)smem_raw;
+    C *aux = A + TS * lda;
+    C *tau = aux + L2::AUX;
+    const int64_t b = blockIdx.y, l = blockIdx.x;
+    V.base += b * a_bstride;
+    ws.nodes += b * ws_bstride;
+    ws.R += b * ws_bstride;
+    ext += b * ws_bstride;
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS;
+    auto house = [](C a, C s, C &bb, C &t, C &sc) { house_scalars(a, s, bb, t, sc); };
+    const int64_t t0 = top + 2 * l, t1 = t0 + 1;
+    const bool two = t1 < top + m;
+    const int64_t c0 = k * TS;
+    for (int idx = tid; idx < 2 * TS * TS; idx += kNTP) {
+        int r, c;
+        if (V.rs == 1) { r = idx % (2 * TS); c = idx / (2 * TS); } else { c = idx % TS; r = idx / TS; }
+        const int64_t gr = (r < TS ? t0 : t1) * TS + (r % TS);
+        A[c * lda + r] = (r < TS || two) ? CV::ld(*V.ptr(gr, c0 + c)) : C(0);
+    }
+    __syncthreads();
+    C *Rg = ws.R + l * ts2;
+    blk::qr_blocked<C, TS, false, kNTP, false, 2 * TS>(A, lda, tau, A, lda, aux, house, [&](int j0) {
+        for (int idx = tid; idx < TS * NB; idx += kNTP) {
+            const int c = j0 + idx / TS, r = idx % TS;
+            Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
+        }
+        __syncthreads();
+    });
+    C *Vk = ws.Vk(l), *V2 = ext + l * 2 * ts2;
+    for (int idx = tid; idx < TS * TS; idx += kNTP) {
+        const int r = idx / TS, i = idx % TS;
+        Vk[idx] = (r > i) ? A[i * lda + r] : (r == i ? C(1) : C(0));
+        V2[idx] = A[i * lda + TS + r];
+    }
+    for (int i = tid; i < TS; i += kNTP) ws.Tt(l)[i] = tau[i];
+    if (m2 == 1) {                        // the super-leaf is the root
+        __syncthreads();
+        write_root_R<S, C, TS>(V, Rg, top, k);
+    }
+}
+
+// T and U of two-tile leaves: G = V^T V over 2ts rows, T by recursive
+// merging, U = V T^T (rows 0..ts-1 into Um, ts..2ts-1 into the leaf2 region).
+template <typename C, int TS>
+struct NodeTU2 {
+    static constexpr int LD = 2 * TS + 1, LT = TS + 1;
+    static constexpr size_t smem = (size_t)(TS * LD + TS * LT + TS * TS / 4 + TS) * sizeof(C);
+};
+template <typename C, int TS>
+__global__ void __launch_bounds__(kNTP) k_node_tu2(C *nodes, C *ext, int64_t ws_bstride) {
+    using NT_ = NodeTU2<C, TS>;
+    constexpr int LD = NT_::LD, LT = NT_::LT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *Vs = (C *)smem_raw;                 // Vs[i * LD + r] = V(r, i), r < 2 TS
+    C *Ts = Vs + TS * LD;                  // Ts[j * LT + i] = T(i, j)
+    C *tmp = Ts + TS * LT;
+    C *tau = tmp + TS * TS / 4;
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS, l = blockIdx.x;
+    C *base = nodes + blockIdx.y * ws_bstride + l * 3 * ts2;
+    C *Vk = base, *Um = base + ts2, *Tt = base + 2 * ts2;
+    C *V2 = ext + blockIdx.y * ws_bstride + l * 2 * ts2, *U2 = V2 + ts2;
+    for (int idx = tid; idx < TS * TS; idx += kNTP) {
+        const int r = idx / TS, i = idx % TS;
+        Vs[i * LD + r] = __ldcg(Vk + idx);
+        Vs[i * LD + TS + r] = __ldcg(V2 + idx);
+    }
+    for (int i = tid; i < TS; i += kNTP) tau[i] = __ldcg(Tt + i);
+    __syncthreads();
+    blk::sgemm<C, 4, 4, kNTP>(TS, TS, 2 * TS,
+        [&](int i, int r) { return Vs[i * LD + r]; },
+        [&](int r, int j) { return Vs[j * LD + r]; },
+        [&](int i, int j, C v) { if (i < j) Ts[j * LT + i] = v; });
+    __syncthreads();
+    panel::build_T_rec<C, TS, kNTP>(tau, tmp, [&](int i, int j) -> C & { return Ts[j * LT + i]; });
+    __syncthreads();
+    // U(r, i) = sum_{j >= i} V(r, j) T(i, j)
+    blk::sgemm<C, 4, 4, kNTP>(2 * TS, TS, TS,
+        [&](int r, int j) { return Vs[j * LD + r]; },
+        [&](int j, int i) { return j >= i ? Ts[j * LT + i] : C(0); },
+        [&](int r, int i, C v) {
+            if (r < TS) Um[i * TS + r] = v; else U2[i * TS + (r - TS)] = v;
+        });
+}
+
 // TT nodes of level j: grid (pairs, batch); node p combines the R factors of
 // leaves a = (2p) << (j-1) and bb = (2p+1) << (j-1).
 template <typename S, typename C, int TS, bool DEFER>
@@ -1010,6 +1125,21 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         cudaDeviceGetStreamPriorityRange(&plo, &phi);
         if ((err = cudaStreamCreateWithPriority(&st3, cudaStreamNonBlocking, phi)) != cudaSuccess) return err;
     }
+    // two-tile leaves (fp32 compute, ts = 128, FMA update path)
+    C *ext = ws.nodes + tree_leaf2_offset<C>(N, TS);
+    bool leaf2 = false;
+    if constexpr (Leaf2<C, TS>::ok && NodeTU2<C, TS>::smem <= 227 * 1024)
+        leaf2 = DEFER && !use_tc && !(getenv("BSVD_LEAF2") && atoi(getenv("BSVD_LEAF2")) == 0);
+    if (leaf2) {
+        static bool set2 = false;
+        if (!set2) {
+            if ((err = cudaFuncSetAttribute(k_panel_leaf2<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Leaf2<C, TS>::smem)) != cudaSuccess) return err;
+            if ((err = cudaFuncSetAttribute(k_node_tu2<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NodeTU2<C, TS>::smem)) != cudaSuccess) return err;
+            set2 = true;
+        }
+    }
+    bool l2side = false;                                // the current side uses two-tile leaves
+    int64_t mtiles = 0;                                 // its panel's tile rows
     const int Lmax0 = tree_levels(N);
     std::vector<cudaEvent_t> tuev(Lmax0 + 1);
     for (auto &e : tuev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -1021,7 +1151,16 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
             return cudaSuccess;
         }
         cudaStreamWaitEvent(st3, (*lvlp)[j], 0);
-        if ((e2 = node_tu(slot0, count, tt, st3)) != cudaSuccess) return e2;
+        if (l2side && j == 0) {
+            if constexpr (Leaf2<C, TS>::ok) {
+                k_node_tu2<C, TS><<<dim3((unsigned)count, (unsigned)batch), kNTP, NodeTU2<C, TS>::smem, st3>>>(
+                    ws.nodes, ext, ws_elems);
+                bsvd_host::count_launch();
+                if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            }
+        } else if ((e2 = node_tu(slot0, count, tt, st3)) != cudaSuccess) {
+            return e2;
+        }
         cudaEventRecord(tuev[j], st3);
         if (tl_side) tlmark("  node_tu", st3);
         cudaStreamWaitEvent(st2, tuev[j], 0);
@@ -1033,7 +1172,8 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                 return launch_apply_level_tc<S>(a, n, batch, a_bstride, lq, top, k, m, (const float *)img,
                                                 ws_elems, j, st2);
         }
-        return launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, j, st2);
+        return launch_apply_level<S, C, TS>(a, n, batch, a_bstride, lq, top, k, m, ws.nodes, ws_elems, j, st2,
+                                            l2side ? ext : nullptr, mtiles);
     };
     auto apply_level = [&](bool lq, int64_t top, int64_t k, int64_t m, int j) -> cudaError_t {
         const cudaError_t e3 = apply_level0(lq, top, k, m, j);
@@ -1062,14 +1202,23 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         const int64_t top = lq ? k + 1 : k;
         if (top >= N) return cudaSuccess;
         const int64_t m = N - top;
-        const int L = tree_levels(m);
+        l2side = leaf2 && m >= 2;
+        mtiles = m;
+        const int64_t mt = l2side ? (m + 1) / 2 : m;      // tree leaves
+        const int L = tree_levels(mt);
         const bool trail = (N - 1 - k) > 0;
         Side sd{};
         cudaStreamWaitEvent(st, done, 0);
         tl_side = (!lq && k == trace_k) ? 1 : 0;
         if (tl_side) tlmark("start", st);
         if (timed) sd.p0 = tmark(st);
-        k_panel_leaf<S, C, TS, DEFER><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, ws, ws_elems, a_bstride);
+        if (l2side) {
+            if constexpr (Leaf2<C, TS>::ok)
+                k_panel_leaf2<S, C, TS><<<dim3((unsigned)mt, (unsigned)batch), kNTP, Leaf2<C, TS>::smem, st>>>(
+                    V, m, mt, top, k, ws, ext, ws_elems, a_bstride);
+        } else {
+            k_panel_leaf<S, C, TS, DEFER><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, ws, ws_elems, a_bstride);
+        }
         bsvd_host::count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -1077,10 +1226,10 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if (tl_side) tlmark("panel leaf", st);
         if (trail) {
             if (timed) sd.t0 = tmark(st2);
-            if ((e = level_tu(0, 0, m, false)) != cudaSuccess) return e;
-            if ((e = apply_level(lq, top, k, m, 0)) != cudaSuccess) return e;
+            if ((e = level_tu(0, 0, mt, false)) != cudaSuccess) return e;
+            if ((e = apply_level(lq, top, k, mt, 0)) != cudaSuccess) return e;
         }
-        int64_t cnt_prev = m;
+        int64_t cnt_prev = mt;
         for (int j = 1; j <= L; ++j) {
             const int64_t pairs = cnt_prev / 2;
             unsigned long long *qtrace = nullptr;
@@ -1090,7 +1239,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                 cudaMemcpyToSymbolAsync(g_panel_trace, &qtrace, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
             }
             if (pairs > 0) {
-                k_panel_tt<S, C, TS, DEFER><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, j, ws, ws_elems, a_bstride);
+                k_panel_tt<S, C, TS, DEFER><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, mt, top, k, j, ws, ws_elems, a_bstride);
                 bsvd_host::count_launch();
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
@@ -1111,10 +1260,10 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                 cudaFree(qtrace);
             }
             if (trail && pairs > 0) {
-                if ((e = level_tu(j, tree_offset(m, j), pairs, true)) != cudaSuccess) return e;
-                if ((e = apply_level(lq, top, k, m, j)) != cudaSuccess) return e;
+                if ((e = level_tu(j, tree_offset(mt, j), pairs, true)) != cudaSuccess) return e;
+                if ((e = apply_level(lq, top, k, mt, j)) != cudaSuccess) return e;
             }
-            cnt_prev = (m + ((int64_t)1 << j) - 1) >> j;
+            cnt_prev = (mt + ((int64_t)1 << j) - 1) >> j;
         }
         if (timed) sd.p1 = tmark(st);
         if (trail) {
