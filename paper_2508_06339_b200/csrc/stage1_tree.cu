@@ -853,7 +853,7 @@ struct Leaf2 {
     static constexpr int LD = 2 * TS + 1;
     static constexpr int AUX = blk::aux_elems<C, TS, 2 * TS>();
     static constexpr size_t smem = (size_t)(TS * LD + AUX + TS + 8) * sizeof(C);
-    static constexpr bool ok = sizeof(C) == 4 && TS == 128 && smem <= 227 * 1024;
+    static constexpr bool ok = sizeof(C) == 4 && TS >= 32 && smem <= 227 * 1024;
 };
 
 template <typename S, typename C, int TS>
