@@ -1233,7 +1233,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         for (int j = 1; j <= L; ++j) {
             const int64_t pairs = cnt_prev / 2;
             unsigned long long *qtrace = nullptr;
-            if (tl_side && j == 1 && pairs > 0) {
+            if (tl_side && j == 1 && pairs > 0 && getenv("BSVD_TT_TRACE")) {
                 cudaMalloc(&qtrace, 256 * 8);
                 cudaMemsetAsync(qtrace, 0, 256 * 8, st);
                 cudaMemcpyToSymbolAsync(g_panel_trace, &qtrace, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
