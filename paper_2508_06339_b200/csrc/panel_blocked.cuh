@@ -94,12 +94,15 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C
     constexpr int NWF = 8;   // measured: 8 warps beat 4 (latency) and 16 (issue)
     constexpr int RPW = R / NWF;
     static_assert(R % NWF == 0, "row list must split evenly over the factor warps");
-    static_assert(NT / 32 >= NWF, "not enough warps");
+    static_assert(NT / 32 > NWF, "not enough warps (the factor warps plus one T warp)");
     const int warp = threadIdx.x >> 5, c = threadIdx.x & 31;
+    // T_sub is built in CHUNKS of columns by warp NWF while the factorisation
+    // runs: warp 0 signals chunk q on named barrier 2 + q (warp 0 + warp NWF)
+    constexpr int CHUNK = NB >= 8 ? NB / 4 : NB;
     if (warp < NWF) {
+        auto fbar = []() { asm volatile("bar.sync 1, %0;" ::"n"(NWF * 32) : "memory"); };
         const int i0 = warp * RPW;
         auto row = [](int i) { return TT ? (i < NB ? J0 + i : TS + (i - NB)) : (J0 + i); };
-        auto fbar = []() { asm volatile("bar.sync 1, %0;" ::"n"(NWF * 32) : "memory"); };
         C x[RPW];
 #pragma unroll
         for (int q = 0; q < RPW; ++q) x[q] = (c < NB) ? A[(J0 + c) * lda + row(i0 + q)] : C(0);
@@ -158,11 +161,15 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C
             fbar();
             // lanes c < kl hold v_c (zero off its support) exactly where v_kl lives,
             // so their dots are G(c, kl) = v_c^T v_kl: T_sub's Gram matrix for free
-            if (warp == 0 && c < kl) {
-                C g = C(0);
+            if (warp == 0) {
+                if (c < kl) {
+                    C g = C(0);
 #pragma unroll
-                for (int w = 0; w < NWF; ++w) g += dpart[w * 32 + c];
-                gsub[kl * (NB + 1) + c] = g;
+                    for (int w = 0; w < NWF; ++w) g += dpart[w * 32 + c];
+                    gsub[kl * (NB + 1) + c] = g;
+                }
+                if ((kl + 1) % CHUNK == 0)               // G columns of a chunk are out
+                    asm volatile("bar.arrive %0, 64;" ::"r"(2 + kl / CHUNK) : "memory");
             }
             if (c > kl && c < NB) {
                 C dd = C(0);
@@ -178,6 +185,34 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C
 #pragma unroll
         for (int q = 0; q < RPW; ++q)
             if (c < NB) A[(J0 + c) * lda + row(i0 + q)] = x[q];
+    } else if (warp == NWF) {
+        // T_sub column by column while the factorisation runs (LAPACK dlarft's
+        // forward recurrence T(0:kl, kl) = -tau_kl T(0:kl, 0:kl) G(0:kl, kl)),
+        // lane c holding row c of T; it sleeps on its chunk barrier, so only
+        // the last chunk's columns remain once the factorisation ends.
+        C trow[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) trow[j] = C(0);
+#pragma unroll 1
+        for (int q = 0; q < NB / CHUNK; ++q) {
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");   // wait for chunk q
+            for (int kl = q * CHUNK; kl < (q + 1) * CHUNK; ++kl) {
+                const C t = tau[J0 + kl];
+                C acc = C(0);
+#pragma unroll
+                for (int j = 0; j < NB; ++j)
+                    if (j < kl) acc += trow[j] * gsub[kl * (NB + 1) + j];
+                const C tv = c < kl ? -t * acc : (c == kl ? t : C(0));
+#pragma unroll
+                for (int j = 0; j < NB; ++j)
+                    if (j == kl) trow[j] = tv;
+            }
+        }
+        if (c < NB) {
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+                if (c <= j) gsub[j * (NB + 1) + c] = trow[j];
+        }
     }
     __syncthreads();
 }
@@ -198,8 +233,8 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
         subpanel<C, TS, TT, NB, J0, NT, ROWS>(A, lda, tau, red, Vs, tsub, house, st);   // + G into tsub
         stamp(4 * (J0 / NB) + 0);
         save_r(J0);
-        // ---- T_sub = merge(G): the strictly upper G = Vs^T Vs came out of the factorisation
-        panel::build_T_rec<C, NB, NT>(tau + J0, gbuf, [&](int i, int j) -> C & { return tsub[j * LDS + i]; });
+        stamp(4 * (J0 / NB) + 3);
+        // (T_sub is in tsub: built alongside the factorisation from its Gram matrix)
         // ---- T[0:J0, J0:J0+NB] = -T[0:J0,0:J0] (Vprev^T Vs) T_sub
         // (FULL_T = false: only the diagonal blocks, which the factorisation
         // itself needs; k_node_tu builds the rest off the critical path)

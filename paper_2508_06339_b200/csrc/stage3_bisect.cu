@@ -195,11 +195,16 @@ __device__ __forceinline__ double finish_value(const double *__restrict__ ob, in
             double dl = 16.0 * 0x1p-52 * fabs(x) + pivmin;
             for (int rep = 0; rep < 4; ++rep) {
                 const double xl = x - dl, xh = x + dl;
-                if (xl > lo && xl < hi) {
-                    if (negcount(ob, m, xl, pivmin) - n < rank) lo = xl; else hi = xl;
+                const bool inl = xl > lo && xl < hi, inh = xh > lo && xh < hi;
+                int cl = 0, ch = 0;                   // both probes in one pass
+                if (inl && inh) negcount2(ob, m, xl, xh, pivmin, cl, ch);
+                else if (inl) cl = negcount(ob, m, xl, pivmin);
+                else if (inh) ch = negcount(ob, m, xh, pivmin);
+                if (inl) {
+                    if (cl - n < rank) lo = xl; else hi = xl;
                 }
-                if (xh > lo && xh < hi) {
-                    if (negcount(ob, m, xh, pivmin) - n < rank) lo = xh; else hi = xh;
+                if (inh && xh > lo && xh < hi) {
+                    if (ch - n < rank) lo = xh; else hi = xh;
                 }
                 if (hi - lo <= 2.5 * dl) break;
                 dl *= 16.0;
@@ -394,7 +399,11 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
         k_slice<<<dim3((unsigned)((P / 2 + 1 + 127) / 128), (unsigned)batch), 128, 0, st>>>(o2, scal, n, P, cnt);
         bsvd_host::count_launch();
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
-        k_values<OutT><<<dim3((unsigned)((n_out + 127) / 128), (unsigned)batch), 128, 0, st>>>(
+        // small blocks spread the values over every SM
+        // (one warp per block while that leaves SMs idle; batches fill them anyway)
+        const int vb = getenv("BSVD_VALUES_BLOCK") ? atoi(getenv("BSVD_VALUES_BLOCK"))
+                       : (n_out * batch >= 148 * 128 ? 128 : 32);
+        k_values<OutT><<<dim3((unsigned)((n_out + vb - 1) / vb), (unsigned)batch), vb, 0, st>>>(
             o2, scal, cnt, P, n, n_out, out, out_stride);
         bsvd_host::count_launch();
         return cudaGetLastError();
