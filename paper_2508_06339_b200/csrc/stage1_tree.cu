@@ -856,7 +856,7 @@ struct Leaf2 {
     static constexpr bool ok = sizeof(C) == 4 && TS >= 32 && smem <= 227 * 1024;
 };
 
-template <typename S, typename C, int TS>
+template <typename S, typename C, int TS, bool FULLT>
 __global__ void __launch_bounds__(kNTP) k_panel_leaf2(View<S> V, int64_t m, int64_t m2, int64_t top,
                                                      int64_t k, TreeWs<C> ws, C *ext,
                                                      int64_t ws_bstride, int64_t a_bstride) {
@@ -887,7 +887,10 @@ __global__ void __launch_bounds__(kNTP) k_panel_leaf2(View<S> V, int64_t m, int6
     }
     __syncthreads();
     C *Rg = ws.R + l * ts2;
-    blk::qr_blocked<C, TS, false, kNTP, false, 2 * TS>(A, lda, tau, A, lda, aux, house, [&](int j0) {
+    // FULLT: the whole compact-WY T comes out of the factorisation, so the
+    // leaf update waits only for the short U = V T^T kernel (k_leaf2_u);
+    // otherwise k_node_tu2 builds T and U (less work in total: batches)
+    blk::qr_blocked<C, TS, false, kNTP, FULLT, 2 * TS>(A, lda, tau, A, lda, aux, house, [&](int j0) {
         for (int idx = tid; idx < TS * NB; idx += kNTP) {
             const int c = j0 + idx / TS, r = idx % TS;
             Rg[c * TS + r] = (r <= c) ? A[c * lda + r] : C(0);
@@ -900,7 +903,15 @@ __global__ void __launch_bounds__(kNTP) k_panel_leaf2(View<S> V, int64_t m, int6
         Vk[idx] = (r > i) ? A[i * lda + r] : (r == i ? C(1) : C(0));
         V2[idx] = A[i * lda + TS + r];
     }
-    for (int i = tid; i < TS; i += kNTP) ws.Tt(l)[i] = tau[i];
+    C *Tg = ws.Tt(l);
+    if constexpr (FULLT) {                // T (column-major, upper; zeros below)
+        for (int idx = tid; idx < TS * TS; idx += kNTP) {
+            const int jj = idx / TS, i = idx % TS;
+            Tg[idx] = (i <= jj) ? A[jj * lda + i] : C(0);
+        }
+    } else {
+        for (int i = tid; i < TS; i += kNTP) Tg[i] = tau[i];
+    }
     if (m2 == 1) {                        // the super-leaf is the root
         __syncthreads();
         write_root_R<S, C, TS>(V, Rg, top, k);
@@ -948,6 +959,45 @@ __global__ void __launch_bounds__(kNTP) k_node_tu2(C *nodes, C *ext, int64_t ws_
         [&](int j, int i) { return j >= i ? Ts[j * LT + i] : C(0); },
         [&](int r, int i, C v) {
             if (r < TS) Um[i * TS + r] = v; else U2[i * TS + (r - TS)] = v;
+        });
+}
+
+// U = V T^T of two-tile leaves from the full T their panel kernel wrote:
+// grid (leaves, U2_SLICES, batch), each CTA a slice of the 2ts rows.
+constexpr int kU2Slices = 4;
+template <typename C, int TS>
+struct LeafU2 {
+    static constexpr int RS = 2 * TS / kU2Slices;         // rows per CTA
+    static constexpr int LT = TS + 1, LV = RS + 1;
+    static constexpr size_t smem = (size_t)(TS * LT + TS * LV) * sizeof(C);
+};
+template <typename C, int TS>
+__global__ void __launch_bounds__(kNTP) k_leaf2_u(C *nodes, C *ext, int64_t ws_bstride) {
+    using LU = LeafU2<C, TS>;
+    constexpr int RS = LU::RS, LT = LU::LT, LV = LU::LV;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *Ts = (C *)smem_raw;                 // Ts[j * LT + i] = T(i, j)
+    C *Vs = Ts + TS * LT;                  // Vs[j * LV + r] = V(r0 + r, j)
+    const int tid = threadIdx.x;
+    const int64_t ts2 = (int64_t)TS * TS, l = blockIdx.x;
+    const int r0 = blockIdx.y * RS;
+    C *base = nodes + blockIdx.z * ws_bstride + l * 3 * ts2;
+    const C *Vk = base, *Tg = base + 2 * ts2;
+    C *Um = base + ts2;
+    C *V2 = ext + blockIdx.z * ws_bstride + l * 2 * ts2, *U2 = V2 + ts2;
+    for (int idx = tid; idx < TS * TS; idx += kNTP) Ts[(idx / TS) * LT + idx % TS] = __ldcg(Tg + idx);
+    for (int idx = tid; idx < RS * TS; idx += kNTP) {
+        const int r = idx / TS, j = idx % TS, gr = r0 + r;
+        Vs[j * LV + r] = gr < TS ? __ldcg(Vk + gr * TS + j) : __ldcg(V2 + (gr - TS) * TS + j);
+    }
+    __syncthreads();
+    // U(r, i) = sum_{j >= i} V(r, j) T(i, j)
+    blk::sgemm<C, 4, 4, kNTP>(RS, TS, TS,
+        [&](int r, int j) { return Vs[j * LV + r]; },
+        [&](int j, int i) { return j >= i ? Ts[j * LT + i] : C(0); },
+        [&](int r, int i, C v) {
+            const int gr = r0 + r;
+            if (gr < TS) Um[i * TS + gr] = v; else U2[i * TS + (gr - TS)] = v;
         });
 }
 
@@ -1128,12 +1178,17 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     // two-tile leaves (fp32 compute, ts = 128, FMA update path)
     C *ext = ws.nodes + tree_leaf2_offset<C>(N, TS);
     bool leaf2 = false;
-    if constexpr (Leaf2<C, TS>::ok && NodeTU2<C, TS>::smem <= 227 * 1024)
+    // one matrix: full T in the leaf panel + short U kernel (the leaf update's
+    // critical path); batches: k_node_tu2 (less work in total)
+    const bool leaf_fullt = batch == 1;
+    if constexpr (Leaf2<C, TS>::ok && NodeTU2<C, TS>::smem <= 227 * 1024 && LeafU2<C, TS>::smem <= 227 * 1024)
         leaf2 = DEFER && !use_tc && !(getenv("BSVD_LEAF2") && atoi(getenv("BSVD_LEAF2")) == 0);
     if (leaf2) {
         static bool set2 = false;
         if (!set2) {
-            if ((err = cudaFuncSetAttribute(k_panel_leaf2<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Leaf2<C, TS>::smem)) != cudaSuccess) return err;
+            if ((err = cudaFuncSetAttribute(k_panel_leaf2<S, C, TS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Leaf2<C, TS>::smem)) != cudaSuccess) return err;
+            if ((err = cudaFuncSetAttribute(k_panel_leaf2<S, C, TS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Leaf2<C, TS>::smem)) != cudaSuccess) return err;
+            if ((err = cudaFuncSetAttribute(k_leaf2_u<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LeafU2<C, TS>::smem)) != cudaSuccess) return err;
             if ((err = cudaFuncSetAttribute(k_node_tu2<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NodeTU2<C, TS>::smem)) != cudaSuccess) return err;
             set2 = true;
         }
@@ -1151,10 +1206,15 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
             return cudaSuccess;
         }
         cudaStreamWaitEvent(st3, (*lvlp)[j], 0);
+        if (tl_side) tlmark("  pre tu", st3);
         if (l2side && j == 0) {
             if constexpr (Leaf2<C, TS>::ok) {
-                k_node_tu2<C, TS><<<dim3((unsigned)count, (unsigned)batch), kNTP, NodeTU2<C, TS>::smem, st3>>>(
-                    ws.nodes, ext, ws_elems);
+                if (leaf_fullt)
+                    k_leaf2_u<C, TS><<<dim3((unsigned)count, kU2Slices, (unsigned)batch), kNTP, LeafU2<C, TS>::smem, st3>>>(
+                        ws.nodes, ext, ws_elems);
+                else
+                    k_node_tu2<C, TS><<<dim3((unsigned)count, (unsigned)batch), kNTP, NodeTU2<C, TS>::smem, st3>>>(
+                        ws.nodes, ext, ws_elems);
                 bsvd_host::count_launch();
                 if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
             }
@@ -1176,6 +1236,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                                             l2side ? ext : nullptr, mtiles);
     };
     auto apply_level = [&](bool lq, int64_t top, int64_t k, int64_t m, int j) -> cudaError_t {
+        if (tl_side) tlmark("    pre apply", st2);
         const cudaError_t e3 = apply_level0(lq, top, k, m, j);
         if (tl_side) tlmark("    apply", st2);
         return e3;
@@ -1214,8 +1275,14 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if (timed) sd.p0 = tmark(st);
         if (l2side) {
             if constexpr (Leaf2<C, TS>::ok)
-                k_panel_leaf2<S, C, TS><<<dim3((unsigned)mt, (unsigned)batch), kNTP, Leaf2<C, TS>::smem, st>>>(
-                    V, m, mt, top, k, ws, ext, ws_elems, a_bstride);
+            {
+                if (leaf_fullt)
+                    k_panel_leaf2<S, C, TS, true><<<dim3((unsigned)mt, (unsigned)batch), kNTP, Leaf2<C, TS>::smem, st>>>(
+                        V, m, mt, top, k, ws, ext, ws_elems, a_bstride);
+                else
+                    k_panel_leaf2<S, C, TS, false><<<dim3((unsigned)mt, (unsigned)batch), kNTP, Leaf2<C, TS>::smem, st>>>(
+                        V, m, mt, top, k, ws, ext, ws_elems, a_bstride);
+            }
         } else {
             k_panel_leaf<S, C, TS, DEFER><<<dim3((unsigned)m, (unsigned)batch), kNTP, psm, st>>>(V, m, top, k, ws, ws_elems, a_bstride);
         }
@@ -1238,6 +1305,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                 cudaMemsetAsync(qtrace, 0, 256 * 8, st);
                 cudaMemcpyToSymbolAsync(g_panel_trace, &qtrace, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
             }
+            if (tl_side) tlmark("pre tt", st);
             if (pairs > 0) {
                 k_panel_tt<S, C, TS, DEFER><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, mt, top, k, j, ws, ws_elems, a_bstride);
                 bsvd_host::count_launch();
