@@ -1141,6 +1141,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     if (psm > set) {
         if ((err = cudaFuncSetAttribute(k_panel_leaf<S, C, TS, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
         if ((err = cudaFuncSetAttribute(k_panel_tt<S, C, TS, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
+        if ((err = cudaFuncSetAttribute(k_panel_tt<S, C, TS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
         if (DEFER && (err = cudaFuncSetAttribute(k_node_tu<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NodeTU<C, TS>::smem)) != cudaSuccess) return err;
         set = psm;
     }
@@ -1180,7 +1181,10 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     bool leaf2 = false;
     // one matrix: full T in the leaf panel + short U kernel (the leaf update's
     // critical path); batches: k_node_tu2 (less work in total)
-    const bool leaf_fullt = batch == 1;
+    // (only while the panel has many tile rows: then the update chain, not
+    // the panel chain, bounds the side, and the leaf's full T pays off)
+    static const int64_t ft_min = getenv("BSVD_LEAF_FT_MIN") ? atoll(getenv("BSVD_LEAF_FT_MIN")) : 32;
+    bool leaf_fullt = false;
     if constexpr (Leaf2<C, TS>::ok && NodeTU2<C, TS>::smem <= 227 * 1024 && LeafU2<C, TS>::smem <= 227 * 1024)
         leaf2 = DEFER && !use_tc && !(getenv("BSVD_LEAF2") && atoi(getenv("BSVD_LEAF2")) == 0);
     if (leaf2) {
@@ -1264,6 +1268,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if (top >= N) return cudaSuccess;
         const int64_t m = N - top;
         l2side = leaf2 && m >= 2;
+        leaf_fullt = batch == 1 && m >= ft_min;
         mtiles = m;
         const int64_t mt = l2side ? (m + 1) / 2 : m;      // tree leaves
         const int L = tree_levels(mt);
@@ -1306,7 +1311,14 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                 cudaMemcpyToSymbolAsync(g_panel_trace, &qtrace, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
             }
             if (tl_side) tlmark("pre tt", st);
-            if (pairs > 0) {
+            // the root node builds its full T itself: no factor kernel between
+            // the last panel node and the update the next side waits for
+            const bool root_full = DEFER && !use_tc && j == L && pairs == 1 && batch == 1;
+            if (root_full) {
+                k_panel_tt<S, C, TS, false><<<dim3(1u, (unsigned)batch), kNTP, psm, st>>>(V, mt, top, k, j, ws, ws_elems, a_bstride);
+                bsvd_host::count_launch();
+                if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            } else if (pairs > 0) {
                 k_panel_tt<S, C, TS, DEFER><<<dim3((unsigned)pairs, (unsigned)batch), kNTP, psm, st>>>(V, mt, top, k, j, ws, ws_elems, a_bstride);
                 bsvd_host::count_launch();
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1328,7 +1340,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
                 cudaFree(qtrace);
             }
             if (trail && pairs > 0) {
-                if ((e = level_tu(j, tree_offset(mt, j), pairs, true)) != cudaSuccess) return e;
+                if ((e = level_tu(j, tree_offset(mt, j), root_full ? 0 : pairs, true)) != cudaSuccess) return e;
                 if ((e = apply_level(lq, top, k, mt, j)) != cudaSuccess) return e;
             }
             cnt_prev = (mt + ((int64_t)1 << j) - 1) >> j;
