@@ -104,10 +104,23 @@ __device__ __forceinline__ void gemm(const C *__restrict__ Ag, const C *Bs, C *A
     constexpr int CH = KC * TS;                       // elements per chunk
     constexpr int PER16 = 16 / (int)sizeof(C);        // elements per 16 B
     constexpr int NV = CH / PER16;                    // 16 B granules per chunk
+    // Triangular operands on the balanced layout: chunk ch holds the
+    // interleaved rows k = NCH i + ch, so every chunk has the same zero profile
+    // and each warp skips the same share of every chunk (contiguous chunks
+    // leave the barrier waiting on the warp whose rows are all nonzero there).
+    constexpr bool ILV = TRI != 0 && G::BAL && KC == 32 && NCH == 4;
     auto issue = [&](int ch) {
         C *dst = Abuf + (ch & 1) * CH;
-        const C *src = Ag + (size_t)ch * CH;
-        for (int v = threadIdx.x; v < NV; v += kNT) cp_async16(dst + v * PER16, src + v * PER16);
+        if constexpr (ILV) {
+            constexpr int GR = TS / PER16;                // granules per row
+            for (int v = threadIdx.x; v < NV; v += kNT) {
+                const int i = v / GR, gc = v % GR;
+                cp_async16(dst + i * TS + gc * PER16, Ag + (size_t)(NCH * i + ch) * TS + gc * PER16);
+            }
+        } else {
+            const C *src = Ag + (size_t)ch * CH;
+            for (int v = threadIdx.x; v < NV; v += kNT) cp_async16(dst + v * PER16, src + v * PER16);
+        }
         cp_async_commit();
     };
     issue(0);
@@ -121,8 +134,80 @@ __device__ __forceinline__ void gemm(const C *__restrict__ Ag, const C *Bs, C *A
         }
         __syncthreads();
         const C *As = Abuf + (ch & 1) * CH;
-        const C *Bk = Bs + (size_t)ch * KC * bnp;
         constexpr int H = G::MR / 2;
+        if constexpr (ILV) {
+            // i ranges (k = NCH i + ch) where each half-block of rows is nonzero
+            constexpr int HB = G::BM / (2 * G::WGM);
+            const int ha = ln.wm, hb = 2 * G::WGM - 1 - ln.wm;
+            auto cnt_le = [&](int kmax) { return kmax < ch ? 0 : min(KC, (kmax - ch) / NCH + 1); };   // #{i: k <= kmax}
+            auto cnt_lt = [&](int kmin) { return kmin <= ch ? 0 : min(KC, (kmin - ch + NCH - 1) / NCH); };   // #{i: k < kmin}
+            int alo = 0, ahi = KC, blo = 0, bhi = KC;
+            if constexpr (TRI == 1) { ahi = cnt_le(HB * ha + HB - 1); bhi = cnt_le(HB * hb + HB - 1); }
+            else { alo = cnt_lt(HB * ha); blo = cnt_lt(HB * hb); }
+            const int b0 = max(alo, blo), b1 = min(ahi, bhi);
+            auto full = [&](int i0, int i1) {
+#pragma unroll 4
+                for (int i = i0; i < i1; ++i) {
+                    const int k = NCH * i + ch;
+                    C a[G::MR], b[G::NR];
+#pragma unroll
+                    for (int t = 0; t < H; ++t) a[t] = As[i * TS + ln.m0 + t];
+#pragma unroll
+                    for (int t = 0; t < H; ++t) a[H + t] = As[i * TS + ln.m1 + t];
+#pragma unroll
+                    for (int j = 0; j < G::NR; ++j) b[j] = Bs[(size_t)k * bnp + ln.n0 + j];
+#pragma unroll
+                    for (int t = 0; t < G::MR; ++t)
+#pragma unroll
+                        for (int j = 0; j < G::NR; ++j) {
+                            if (NEG) acc[t][j] -= a[t] * b[j];
+                            else acc[t][j] += a[t] * b[j];
+                        }
+                }
+            };
+            auto half = [&](bool second, int i0, int i1) {
+                const int mh = second ? ln.m1 : ln.m0;
+#pragma unroll 4
+                for (int i = i0; i < i1; ++i) {
+                    const int k = NCH * i + ch;
+                    C a[H], b[G::NR];
+#pragma unroll
+                    for (int t = 0; t < H; ++t) a[t] = As[i * TS + mh + t];
+#pragma unroll
+                    for (int j = 0; j < G::NR; ++j) b[j] = Bs[(size_t)k * bnp + ln.n0 + j];
+                    if (second) {
+#pragma unroll
+                        for (int t = 0; t < H; ++t)
+#pragma unroll
+                            for (int j = 0; j < G::NR; ++j) {
+                                if (NEG) acc[H + t][j] -= a[t] * b[j];
+                                else acc[H + t][j] += a[t] * b[j];
+                            }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < H; ++t)
+#pragma unroll
+                            for (int j = 0; j < G::NR; ++j) {
+                                if (NEG) acc[t][j] -= a[t] * b[j];
+                                else acc[t][j] += a[t] * b[j];
+                            }
+                    }
+                }
+            };
+            if (b0 < b1) full(b0, b1);
+            // the rest of each half's range (an interval sharing one end with the overlap)
+            if (alo < ahi) {
+                if (alo < b0) half(false, alo, min(ahi, b0));
+                if (ahi > b1) half(false, max(alo, b1), ahi);
+            }
+            if (blo < bhi) {
+                if (blo < b0) half(true, blo, min(bhi, b0));
+                if (bhi > b1) half(true, max(blo, b1), bhi);
+            }
+            __syncthreads();   // buffer (ch & 1) is refilled by issue(ch + 2)
+            continue;
+        }
+        const C *Bk = Bs + (size_t)ch * KC * bnp;
         bool za = false, zb = false;                      // microtile halves entirely zero
         if constexpr (TRI != 0 && G::BAL && KC == 2 * (G::BM / (2 * G::WGM))) {
             const int ha = ln.wm, hb = 2 * G::WGM - 1 - ln.wm;   // half-block indices

@@ -1179,10 +1179,9 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     // two-tile leaves (fp32 compute, ts = 128, FMA update path)
     C *ext = ws.nodes + tree_leaf2_offset<C>(N, TS);
     bool leaf2 = false;
-    // one matrix: full T in the leaf panel + short U kernel (the leaf update's
-    // critical path); batches: k_node_tu2 (less work in total)
-    // (only while the panel has many tile rows: then the update chain, not
-    // the panel chain, bounds the side, and the leaf's full T pays off)
+    // full T in the leaf panel + short U kernel while the panel has many tile
+    // rows (then the update chain, not the panel chain, bounds the side);
+    // otherwise k_node_tu2 (less work on the panel chain)
     static const int64_t ft_min = getenv("BSVD_LEAF_FT_MIN") ? atoll(getenv("BSVD_LEAF_FT_MIN")) : 32;
     bool leaf_fullt = false;
     if constexpr (Leaf2<C, TS>::ok && NodeTU2<C, TS>::smem <= 227 * 1024 && LeafU2<C, TS>::smem <= 227 * 1024)
@@ -1268,7 +1267,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         if (top >= N) return cudaSuccess;
         const int64_t m = N - top;
         l2side = leaf2 && m >= 2;
-        leaf_fullt = batch == 1 && m >= ft_min;
+        leaf_fullt = m >= ft_min;      // (never batch-dependent: batched == single, bit for bit)
         mtiles = m;
         const int64_t mt = l2side ? (m + 1) / 2 : m;      // tree leaves
         const int L = tree_levels(mt);
@@ -1313,7 +1312,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
             if (tl_side) tlmark("pre tt", st);
             // the root node builds its full T itself: no factor kernel between
             // the last panel node and the update the next side waits for
-            const bool root_full = DEFER && !use_tc && j == L && pairs == 1 && batch == 1;
+            const bool root_full = DEFER && !use_tc && j == L && pairs == 1;
             if (root_full) {
                 k_panel_tt<S, C, TS, false><<<dim3(1u, (unsigned)batch), kNTP, psm, st>>>(V, mt, top, k, j, ws, ws_elems, a_bstride);
                 bsvd_host::count_launch();
