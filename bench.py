@@ -263,7 +263,7 @@ def run_b200(args):
                "(MEASURED_PEAKS.json has no CUDA-core FMA entry)")
     ach1 = flop_model(n) * units / (stage1_ms * 1e-3) / 1e12
     phases = {
-        "stage1": {"bound": "fma", "kernel": "stage 1 (k_panel_leaf/k_panel_tt + k_node_tu + k_apply_leaf/k_apply_tt on 3 streams)",
+        "stage1": {"bound": "fma", "kernel": "stage 1 (k_panel_leaf2/k_panel_tt + k_leaf2_u/k_node_tu + k_apply_leaf2/k_apply_tt on 3 streams)",
                    "achieved": ach1, "peak": fpk, "unit": "TFLOP/s", "frac": ach1 / fpk,
                    "peak_source": fpk_src, "model": "8/3 n^3 flops (the reference's count)", "traffic": None},
     }
