@@ -1182,7 +1182,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     // full T in the leaf panel + short U kernel while the panel has many tile
     // rows (then the update chain, not the panel chain, bounds the side);
     // otherwise k_node_tu2 (less work on the panel chain)
-    static const int64_t ft_min = getenv("BSVD_LEAF_FT_MIN") ? atoll(getenv("BSVD_LEAF_FT_MIN")) : 32;
+    const int64_t ft_min = getenv("BSVD_LEAF_FT_MIN") ? atoll(getenv("BSVD_LEAF_FT_MIN")) : 32;
     bool leaf_fullt = false;
     if constexpr (Leaf2<C, TS>::ok && NodeTU2<C, TS>::smem <= 227 * 1024 && LeafU2<C, TS>::smem <= 227 * 1024)
         leaf2 = DEFER && !use_tc && !(getenv("BSVD_LEAF2") && atoi(getenv("BSVD_LEAF2")) == 0);

@@ -249,3 +249,15 @@ def test_chase_wide_band_batched(P, be_tree, oracle):
     assert np.array_equal(got[2], np.arange(300, 0, -1, dtype=np.float32))
     for i in (0, 1, 3, 4):
         assert_close(got[i], oracle.svdvals(a[i].T.copy(), 128), np.float32, 300, what=f"member {i}")
+
+
+@pytest.mark.parametrize("ft_min", ["2", "1000"])
+@pytest.mark.parametrize("n", [1024, 1152])
+def test_leaf_full_t_paths(P, be_tree, oracle, monkeypatch, n, ft_min):
+    """Two-tile leaves with full T from the panel + k_leaf2_u (FULLT, forced
+    here for every side with BSVD_LEAF_FT_MIN=2; by default only panels of
+    >= 32 tile rows) and the k_node_tu2 path agree with the oracle."""
+    monkeypatch.setenv("BSVD_LEAF_FT_MIN", ft_min)
+    a = np.random.default_rng(n).standard_normal((n, n)).astype(np.float32)
+    got = P.svdvals(a, P.KernelConfig(tilesize=128), backend=be_tree)
+    assert_close(got, oracle.svdvals(a, 128), np.float32, n, what=f"n={n} ft_min={ft_min}")
