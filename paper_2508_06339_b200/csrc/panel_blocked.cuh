@@ -82,6 +82,14 @@ __host__ __device__ constexpr int aux_elems() {
     return (ROWS + NB) * (NB + 1) + 2 * NB * TS + NB * (NB + 1) + 16 * 34 + 8 + (ROWS + 2 * NB);
 }
 
+#ifndef BSVD_NWF_LEAF2
+#define BSVD_NWF_LEAF2 8
+#endif
+// factor warps per sub-panel: measured, 8 beat 4 (latency) and 16 (issue) on
+// ts-row operands
+template <bool TT, int TS, int ROWS>
+__host__ __device__ constexpr int nwf() { return (!TT && ROWS == 2 * TS) ? BSVD_NWF_LEAF2 : 8; }
+
 // Step 1: register-resident factorisation of sub-panel J0 by the first NWF
 // warps (named barrier 1); the remaining warps only join the final barrier.
 // Fewer, fatter warps: the per-step overheads that every warp pays (partial-
@@ -91,10 +99,11 @@ template <typename C, int TS, bool TT, int NB, int J0, int NT, int ROWS, typenam
 __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C *gsub, HS house,
                                          unsigned long long *st) {
     constexpr int R = TT ? (2 * NB + J0) : (ROWS - J0);  // rows in the sub-panel's row list
-    constexpr int NWF = 8;   // measured: 8 warps beat 4 (latency) and 16 (issue)
+    constexpr int NWF = nwf<TT, TS, ROWS>();
+    constexpr bool TW = NT / 32 > NWF;    // a spare warp builds T_sub alongside
     constexpr int RPW = R / NWF;
     static_assert(R % NWF == 0, "row list must split evenly over the factor warps");
-    static_assert(NT / 32 > NWF, "not enough warps (the factor warps plus one T warp)");
+    static_assert(NT / 32 >= NWF, "not enough warps");
     const int warp = threadIdx.x >> 5, c = threadIdx.x & 31;
     // T_sub is built in CHUNKS of columns by warp NWF while the factorisation
     // runs: warp 0 signals chunk q on named barrier 2 + q (warp 0 + warp NWF)
@@ -168,7 +177,7 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C
                     for (int w = 0; w < NWF; ++w) g += dpart[w * 32 + c];
                     gsub[kl * (NB + 1) + c] = g;
                 }
-                if ((kl + 1) % CHUNK == 0)               // G columns of a chunk are out
+                if (TW && (kl + 1) % CHUNK == 0)         // G columns of a chunk are out
                     asm volatile("bar.arrive %0, 64;" ::"r"(2 + kl / CHUNK) : "memory");
             }
             if (c > kl && c < NB) {
@@ -185,7 +194,7 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C
 #pragma unroll
         for (int q = 0; q < RPW; ++q)
             if (c < NB) A[(J0 + c) * lda + row(i0 + q)] = x[q];
-    } else if (warp == NWF) {
+    } else if (TW && warp == NWF) {
         // T_sub column by column while the factorisation runs (LAPACK dlarft's
         // forward recurrence T(0:kl, kl) = -tau_kl T(0:kl, 0:kl) G(0:kl, kl)),
         // lane c holding row c of T; it sleeps on its chunk barrier, so only
@@ -234,7 +243,10 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
         stamp(4 * (J0 / NB) + 0);
         save_r(J0);
         stamp(4 * (J0 / NB) + 3);
-        // (T_sub is in tsub: built alongside the factorisation from its Gram matrix)
+        // (T_sub is in tsub: built alongside the factorisation from its Gram
+        // matrix -- or here, by recursive merging, when no warp was spare)
+        if constexpr (!(NT / 32 > nwf<TT, TS, ROWS>()))
+            panel::build_T_rec<C, NB, NT>(tau + J0, gbuf, [&](int i, int j) -> C & { return tsub[j * LDS + i]; });
         // ---- T[0:J0, J0:J0+NB] = -T[0:J0,0:J0] (Vprev^T Vs) T_sub
         // (FULL_T = false: only the diagonal blocks, which the factorisation
         // itself needs; k_node_tu builds the rest off the critical path)
