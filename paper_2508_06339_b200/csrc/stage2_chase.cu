@@ -726,7 +726,8 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
             unsigned long long *tr =
                 (trace && m == 0 && s < 256 && k < 32 && tid == 0) ? trace + (s * 32 + k) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
-            if (s > 0) {
+            T x[4][8];
+            if (s > 0 && !(strict & 2)) {
                 // sweep s-1 must have stored blocks 0..k (flag 2) and the
                 // edges of blocks k+1, k+2 (flag >= 1): the rows/columns of
                 // this block that lie in them (scripts/chase_dep_check.py);
@@ -734,16 +735,76 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
                 const int lo = k >= NC ? k - NC + 1 : 0;
                 const int j = lo + tid;
                 if (j < min(k + 3, nprev)) {
-                    const int want = (j <= k || strict) ? 2 : 1;
+                    const int want = (j <= k || (strict & 1)) ? 2 : 1;
                     const int *f = fl - fstride + j;
                     for (int spin = 0; ld_acquire(f) < want; ++spin)
                         if (spin > 64) __nanosleep(32);
                 }
                 __syncthreads();
+                load_blk<T>(A, g, x);
+            } else if (s > 0) {
+                // sweep s-1 must have stored blocks 0..k (flag 2) and the
+                // edges of blocks k+1, k+2 (flag >= 1): the rows/columns of
+                // this block that lie in them (scripts/chase_dep_check.py);
+                // blocks below k-NC+1 were checked for this CTA's previous block.
+                // The block is loaded once blocks <= k are stored; the elements
+                // on those two edges (a bit mask over the thread's slots, from
+                // the geometry alone) are reloaded after the edge flags.
+                const int lo = k >= NC ? k - NC + 1 : 0;
+                const int j = lo + tid;
+                if (j <= k && j < nprev) {
+                    const int *f = fl - fstride + j;
+                    for (int spin = 0; ld_acquire(f) < 2; ++spin)
+                        if (spin > 64) __nanosleep(32);
+                }
+                __syncthreads();
+                load_blk<T>(A, g, x);
+                uint32_t mask = 0;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int ke = k + 1 + e;
+                    const Blk ge = geom(s - 1, ke, n, b);
+                    const int dr = (int)(ge.R0 - g.R0), dc = (int)(ge.C0 - g.C0);
+                    if (ke < nprev && !(ke & 1)) {             // row 0 of an even block
+                        if (dr >= 0 && dr < g.nr && (dr & 31) == l) {
+                            const int clo = max(0, dc), chi = min(g.nc, dc + ge.nc);
+                            uint32_t qb = 0;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int c = w + 16 * q;
+                                qb |= (c >= clo && c < chi) ? (1u << q) : 0u;
+                            }
+                            mask |= qb << (8 * (dr >> 5));
+                        }
+                    } else if (ke < nprev) {                   // column 0 of an odd block
+                        if (dc >= 0 && dc < g.nc && (dc & 15) == w) {
+                            const int rlo = max(0, dr), rhi = min(g.nr, dr + ge.nr);
+#pragma unroll
+                            for (int aa = 0; aa < 4; ++aa) {
+                                const int r = l + 32 * aa;
+                                mask |= (r >= rlo && r < rhi) ? (1u << (8 * aa + (dc >> 4))) : 0u;
+                            }
+                        }
+                    }
+                }
+                if (j > k && j < min(k + 3, nprev)) {
+                    const int *f = fl - fstride + j;
+                    for (int spin = 0; ld_acquire(f) < ((strict & 1) ? 2 : 1); ++spin)
+                        if (spin > 64) __nanosleep(32);
+                }
+                __syncthreads();
+                if (mask) {
+#pragma unroll
+                    for (int aa = 0; aa < 4; ++aa)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if ((mask >> (8 * aa + q)) & 1u)
+                                x[aa][q] = __ldcg(A.at(g.R0 + l + 32 * aa, g.C0 + w + 16 * q));
+                }
+            } else {
+                load_blk<T>(A, g, x);
             }
             if (tr) tr[1] = gtimer();
-            T x[4][8];
-            load_blk<T>(A, g, x);
             const T *pv;
             int L;
             if (k == 0) {
@@ -1078,7 +1139,12 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         const int fstride = chase_max_ops(n, b);
         err = cudaMemsetAsync(flags, 0, (size_t)batch * n * fstride * sizeof(int), st);
         if (err != cudaSuccess) return err;
-        const int strict = getenv("BSVD_CHASE_STRICT") ? 1 : 0;
+        // bit 1: load a block before its neighbours' edges land (shorter sweep
+        // interval, more CTA time per block) -- only while the sweeps in flight
+        // (~ ops per sweep / 4) fit in the resident clusters
+        int early = nops0 * batch <= 4 * want ? 2 : 0;
+        if (const char *e = getenv("BSVD_CHASE_EARLY")) early = atoi(e) ? 2 : 0;
+        const int strict = (getenv("BSVD_CHASE_STRICT") ? 1 : 0) | early;
         err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, flags, fstride, nitems, trace, strict);
         bsvd_host::count_launch();
         if (err != cudaSuccess) return err;

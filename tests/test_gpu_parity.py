@@ -261,3 +261,18 @@ def test_leaf_full_t_paths(P, be_tree, oracle, monkeypatch, n, ft_min):
     a = np.random.default_rng(n).standard_normal((n, n)).astype(np.float32)
     got = P.svdvals(a, P.KernelConfig(tilesize=128), backend=be_tree)
     assert_close(got, oracle.svdvals(a, 128), np.float32, n, what=f"n={n} ft_min={ft_min}")
+
+
+@pytest.mark.parametrize("early", ["0", "1"])
+@pytest.mark.parametrize("n", [257, 640, 1500])
+def test_chase_edge_reload_modes(P, be_tree, oracle, monkeypatch, n, early):
+    """The carried-block chase with a block loaded before (BSVD_CHASE_EARLY=1,
+    the default while the sweeps in flight fit the resident clusters) or after
+    (0) its neighbours' edges land: both give the band's singular values."""
+    monkeypatch.setenv("BSVD_CHASE_EARLY", early)
+    rng = np.random.default_rng(n + 7)
+    a = np.triu(rng.standard_normal((n, n)))
+    a -= np.triu(a, 129)
+    d, e = P.band_to_bidiagonal(a.astype(np.float32), 128, backend=be_tree)
+    want = np.linalg.svd(a, compute_uv=False)
+    assert_close(oracle.bidiagonal_values(d, e), want, np.float32, n, what=f"n={n} early={early}")
