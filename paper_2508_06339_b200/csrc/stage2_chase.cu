@@ -1139,10 +1139,11 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         const int fstride = chase_max_ops(n, b);
         err = cudaMemsetAsync(flags, 0, (size_t)batch * n * fstride * sizeof(int), st);
         if (err != cudaSuccess) return err;
-        // bit 1: load a block before its neighbours' edges land (shorter sweep
-        // interval, more CTA time per block) -- only while the sweeps in flight
-        // (~ ops per sweep / 4) fit in the resident clusters
-        int early = nops0 * batch <= 4 * want ? 2 : 0;
+        // bit 1 (BSVD_CHASE_EARLY=1): load a block before its neighbours' edges
+        // land and reload just those edges after their flags.  Measured: 59.9
+        // vs 58.6 ms at 8192 and 145.7 vs 136.0 ms at 16384 (the extra CTA time
+        // per block costs more than the earlier load saves) -- off by default.
+        int early = 0;
         if (const char *e = getenv("BSVD_CHASE_EARLY")) early = atoi(e) ? 2 : 0;
         const int strict = (getenv("BSVD_CHASE_STRICT") ? 1 : 0) | early;
         err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, flags, fstride, nitems, trace, strict);
