@@ -266,9 +266,9 @@ def test_leaf_full_t_paths(P, be_tree, oracle, monkeypatch, n, ft_min):
 @pytest.mark.parametrize("early", ["0", "1"])
 @pytest.mark.parametrize("n", [257, 640, 1500])
 def test_chase_edge_reload_modes(P, be_tree, oracle, monkeypatch, n, early):
-    """The carried-block chase with a block loaded before (BSVD_CHASE_EARLY=1,
-    the default while the sweeps in flight fit the resident clusters) or after
-    (0, the default) its neighbours' edges land: both give the band's singular values."""
+    """The carried-block chase with a block loaded before (BSVD_CHASE_EARLY=1)
+    or after (0, the default) its neighbours' edges land: both give the band's
+    singular values."""
     monkeypatch.setenv("BSVD_CHASE_EARLY", early)
     rng = np.random.default_rng(n + 7)
     a = np.triu(rng.standard_normal((n, n)))
