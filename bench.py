@@ -271,7 +271,13 @@ def run_b200(args):
     belem = 8 if dtype == torch.float64 else 4
     algo_bytes = 2.0 * bw * npad * npad * belem * units
     ach2 = algo_bytes / (per["bidiagonal"] * 1e-3) / 1e9
-    phases["bidiagonal"] = {"bound": "hbm", "kernel": "k_chase2 (stage 2, carried-block cluster chase, one launch)",
+    if bw > 64:
+        chase_k = "k_chase2 (stage 2, carried-block cluster chase, one launch)"
+    elif units >= 512:
+        chase_k = "k_chase_cta (stage 2, one CTA per matrix, carried blocks in registers)"
+    else:
+        chase_k = "k_chase (stage 2, pipelined cluster chase)"
+    phases["bidiagonal"] = {"bound": "hbm", "kernel": chase_k,
                             "achieved": ach2, "peak": hbm_gbs, "unit": "GB/s", "frac": ach2 / hbm_gbs,
                             "peak_source": peak_src, "algorithmic_bytes": algo_bytes,
                             "model": f"touch model 2*bw*n^2*{belem} B per matrix (SURVEY.md 8(d))", "traffic": None}
