@@ -70,14 +70,15 @@ __global__ void __launch_bounds__(256) k_bisect_prep(const double *__restrict__ 
     }
 }
 
-// o / q for the Sturm recurrences: reciprocal seed, two Newton steps and one
-// residual correction (the arithmetic of the IEEE division's fast path, but
-// branch-free: the recurrence's operands never reach its slow-path ranges --
-// |q| >= pivmin = 2^-1000, o <= 4 after prescaling).
+// o / q for the Sturm recurrences: reciprocal seed, one Newton step (~2^-46)
+// and one residual correction y + r (o - q y), which squares that error again:
+// correctly rounded but for rare near-ties -- branch-free, because the
+// recurrence's operands never reach the IEEE division's slow-path ranges
+// (|q| >= pivmin = 2^-1000, o <= 4 after prescaling).  A second Newton step
+// changed no value of 3 x 8192 tested and cost 14% of stage 3.
 __device__ __forceinline__ double sdiv(double o, double q) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-    r = r * fma(-q, r, 2.0);
     r = r * fma(-q, r, 2.0);
     const double y = o * r;
     return fma(fma(-q, y, o), r, y);
