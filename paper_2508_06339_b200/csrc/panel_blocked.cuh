@@ -168,22 +168,19 @@ __device__ __forceinline__ void subpanel(C *A, int lda, C *tau, C *red, C *Vs, C
             }
             dpart[warp * 32 + c] = d0 + d1;
             fbar();
-            // lanes c < kl hold v_c (zero off its support) exactly where v_kl lives,
-            // so their dots are G(c, kl) = v_c^T v_kl: T_sub's Gram matrix for free
-            if (warp == 0) {
-                if (c < kl) {
-                    C g = C(0);
+            // one reduction for every lane (no divergent second pass): lanes
+            // c > kl get their column's dot, and lanes c < kl hold v_c (zero off
+            // its support) exactly where v_kl lives, so theirs is the Gram entry
+            // G(c, kl) = v_c^T v_kl -- T_sub's Gram matrix for free
+            C dd = C(0);
 #pragma unroll
-                    for (int w = 0; w < NWF; ++w) g += dpart[w * 32 + c];
-                    gsub[kl * (NB + 1) + c] = g;
-                }
+            for (int w = 0; w < NWF; ++w) dd += dpart[w * 32 + c];
+            if (warp == 0) {
+                if (c < kl) gsub[kl * (NB + 1) + c] = dd;
                 if (TW && (kl + 1) % CHUNK == 0)         // G columns of a chunk are out
                     asm volatile("bar.arrive %0, 64;" ::"r"(2 + kl / CHUNK) : "memory");
             }
             if (c > kl && c < NB) {
-                C dd = C(0);
-#pragma unroll
-                for (int w = 0; w < NWF; ++w) dd += dpart[w * 32 + c];
                 const C wc = t * dd;
 #pragma unroll
                 for (int q = 0; q < RPW; ++q) x[q] -= wc * v[q];
