@@ -238,15 +238,17 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
         };
         subpanel<C, TS, TT, NB, J0, NT, ROWS>(A, lda, tau, red, Vs, tsub, house, st);   // + G into tsub
         stamp(4 * (J0 / NB) + 0);
-        save_r(J0);
+        // FULL_T: T's blocks overwrite R's rows in place, so R leaves first;
+        // otherwise nothing overwrites R and qr_blocked saves it once at the end
+        if constexpr (FULL_T) save_r(J0);
         stamp(4 * (J0 / NB) + 3);
         // (T_sub is in tsub: built alongside the factorisation from its Gram
         // matrix -- or here, by recursive merging, when no warp was spare)
         if constexpr (!(NT / 32 > nwf<TT, TS, ROWS>()))
             panel::build_T_rec<C, NB, NT>(tau + J0, gbuf, [&](int i, int j) -> C & { return tsub[j * LDS + i]; });
         // ---- T[0:J0, J0:J0+NB] = -T[0:J0,0:J0] (Vprev^T Vs) T_sub
-        // (FULL_T = false: only the diagonal blocks, which the factorisation
-        // itself needs; k_node_tu builds the rest off the critical path)
+        // (FULL_T = false: none -- the sub-panel updates use T_sub from tsub,
+        // and k_node_tu builds T off the critical path)
         if constexpr (J0 > 0 && FULL_T) {
             // only rows where both can be nonzero: LEAF rows [J0,TS); TT bottom rows [0, J0+NB)
             constexpr int KLO = TT ? NB : 0;
@@ -265,11 +267,13 @@ __device__ __forceinline__ void qr_step(C *A, int lda, C *tau, C *Tm, int ldt, C
                 [&](int q, int a) { return wbuf[a * TS + q]; },
                 [&](int p, int a, C v) { Tm[(J0 + a) * ldt + p] = -v; });
         }
-        for (int idx = threadIdx.x; idx < NB * NB; idx += NT) {
-            const int a = idx % NB, b = idx / NB;
-            if (a <= b) Tm[(J0 + b) * ldt + (J0 + a)] = tsub[b * LDS + a];
+        if constexpr (FULL_T) {                     // (the updates below read tsub)
+            for (int idx = threadIdx.x; idx < NB * NB; idx += NT) {
+                const int a = idx % NB, b = idx / NB;
+                if (a <= b) Tm[(J0 + b) * ldt + (J0 + a)] = tsub[b * LDS + a];
+            }
+            __syncthreads();
         }
-        __syncthreads();
         stamp(4 * (J0 / NB) + 1);
         // ---- apply the sub-panel block reflector to columns [J0+NB, TS)
         constexpr int NCOL = TS - J0 - NB;
@@ -299,6 +303,8 @@ template <typename C, int TS, bool TT, int NT, bool FULL_T = true, int ROWS = TS
 __device__ void qr_blocked(C *A, int lda, C *tau, C *Tm, int ldt, C *aux, HS house, SaveR save_r,
                            unsigned long long *st = nullptr) {
     qr_step<C, TS, TT, NBsel<C, TS>::v, 0, NT, FULL_T, ROWS>(A, lda, tau, Tm, ldt, aux, house, save_r, st);
+    if constexpr (!FULL_T)
+        for (int j0 = 0; j0 < TS; j0 += NBsel<C, TS>::v) save_r(j0);
 }
 
 }  // namespace blk
