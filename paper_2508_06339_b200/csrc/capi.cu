@@ -58,6 +58,8 @@ bsvd_config resolve_cfg(const bsvd_config *cfg, int64_t n) {
     return c;
 }
 
+bool use_flat(bsvd_dtype dt, int ts) { return flat_supported(ts, dt == BSVD_FP64 ? 8 : 4); }
+
 struct Plan {
     int64_t n, N, np, batch;
     int ts;
@@ -83,6 +85,7 @@ Plan make_plan(bsvd_dtype dt, int64_t n, int64_t batch, const bsvd_config &c, in
         default: s1 = tree_workspace_bytes<__half, float>(p.np, p.ts); break;
         }
         s1 *= (size_t)batch;
+        if (use_flat(dt, p.ts)) s1 = std::max(s1, flat_workspace_bytes(p.np, p.ts, batch));
     }
     p.stage1_bytes = align_up(s1);
     p.chase_bytes = align_up(chase_workspace_bytes(p.np, p.ts, batch));
@@ -118,8 +121,18 @@ bsvd_status stage1(S *work, const Plan &p, const bsvd_config &c, int algo, char 
         }
         return BSVD_OK;
     }
-    cudaEvent_t evp[2], evt[2];
     double pms = 0, tms = 0;
+    if (sizeof(C) == 4 && flat_supported(p.ts, 4)) {
+        e = banddiag_flat<S>(work, p.np, p.ts, p.batch, p.np * p.np, scratch, st, timers ? &pms : nullptr,
+                             timers ? &tms : nullptr);
+        if (timers) {
+            timers->panel_s += pms * 1e-3;
+            timers->trailing_s += tms * 1e-3;
+        }
+        if (e != cudaSuccess) return cuda_error(e, "stage 1 (flat)");
+        return BSVD_OK;
+    }
+    cudaEvent_t evp[2], evt[2];
     if (timers) {
         for (int i = 0; i < 2; ++i) {
             cudaEventCreate(&evp[i]);

@@ -43,6 +43,14 @@ cudaError_t banddiag_tree(S *a, int64_t n, int ts, int64_t batch, int64_t a_bstr
                           cudaStream_t st, cudaEvent_t *ev_panel, cudaEvent_t *ev_trail,
                           double *panel_ms, double *trail_ms);
 
+// ---- stage1_flat.cu (flat cluster panel + one compact-WY update per side) --
+// fp32 compute (FP32 / FP16 storage), ts in {64, 128}.
+bool flat_supported(int ts, int elem_bytes);
+size_t flat_workspace_bytes(int64_t n, int ts, int64_t batch);
+template <typename S>
+cudaError_t banddiag_flat(S *a, int64_t n, int ts, int64_t batch, int64_t a_bstride, void *ws,
+                          cudaStream_t st, double *panel_ms, double *trail_ms);
+
 // ---- stage1_apply.cu (per-level WY trailing updates, ts >= 16) ----------
 template <typename S, typename C, int TS>
 cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride, bool lq,

@@ -1,0 +1,1143 @@
+// stage1_flat.cu -- stage 1 (dense -> band) as ONE flat Householder panel and
+// ONE compact-WY trailing update per sweep side, fp32 compute (FP32 and FP16
+// storage), ts in {64, 128}.
+//
+// Same sweep structure and tile operators as the reference stage 1
+// (bandreduce.py:31-120 getsmqrt / banddiag; kernels.py:205-421 geqrt,
+// tsqrt, unmqr, tsmqr): per sweep side (RQ on the matrix, LQ on its lazy
+// transpose -- a stride swap, no copy) the panel -- view tile column k, tile
+// rows top..N-1, M = (N-top)*ts rows -- is reduced to [R; 0] by ts
+// Householder reflectors, and the trailing columns X (M x C) are replaced by
+// Q^T X.  The reference factors the panel as a flat TSQRT chain of tile QRs
+// and applies it tile by tile (4*ts flops per column per reflector,
+// kernels.py:180-188); here the panel is one Householder QR of the whole
+// M x ts block and the update is the aggregated compact-WY form
+//     W = V^T X,  W2 = T^T W,  X -= V W2             (4*M*ts*C flops)
+// -- the reference's algorithmic flop count, no tree-level
+// overhead, two GEMM-shaped products per side.  The orthogonal factor is the
+// panel's (unique up to signs) Householder QR; the band differs from the
+// reference's tile-chain band by those signs only, the values do not.
+//
+// Kernels per side (streams: P = high priority panel chain, U = update):
+//   k_fpanel  [P]  one thread-block cluster (<= 16 CTAs, rows split across
+//                  CTAs, 512 threads each).  32-column sub-panels live in
+//                  registers; per column ONE cluster-wide reduction (the dot
+//                  products of the pivot column with every sub-panel column,
+//                  which yield the norm, the update coefficients and the
+//                  V^T v column of T at once) pushed through DSMEM; the rest
+//                  of the panel gets the sub-panel's block reflector.  Writes
+//                  R in place, V (fp32, row- and column-major) and tau.
+//   k_fgram   [P]  G = V^T V split over rows, the last CTA merges the parts in
+//                  a fixed order and builds T (recursive larft).  Overlaps
+//                  k_fgemm1.
+//   k_fgemm1  [U]  W_s = V[rows_s]^T X[rows_s]  (split-K partials).
+//   k_fw2x1   [P]  W2 = T^T sum_s W_s; X[0:ts] -= V[0:ts] W2 -- the top tile
+//                  row is the NEXT side's panel, so it is finished first
+//                  (look-ahead) and the next panel starts while ...
+//   k_fgemm2  [U]  X[ts:M] -= V[ts:M] W2  runs on the other stream.
+// All reductions have a fixed order (deterministic, no float atomics).
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "panel_qr.cuh"
+
+namespace bsvd {
+namespace flat {
+
+constexpr int NB = 32;       // sub-panel width (columns held in registers)
+constexpr int kPT = 512;     // panel threads: 128 row groups x 4 column groups
+constexpr int kMaxCS = 16;   // cluster size limit (non-portable)
+constexpr int kGT = 256;     // GEMM threads
+constexpr int KC = 16;       // GEMM k-chunk
+constexpr int kMaxSplit = 16;
+
+// ---------------------------------------------------------------------------
+// storage helpers (FP16 = storage only: widen on load, round-to-nearest on store)
+__device__ __forceinline__ float ldf(const float *p) { return *p; }
+__device__ __forceinline__ float ldf(const __half *p) { return __half2float(*p); }
+__device__ __forceinline__ void stf(float *p, float v) { *p = v; }
+__device__ __forceinline__ void stf(__half *p, float v) { *p = __float2half_rn(v); }
+__device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ float4 ld4(const __half *p) {
+    const uint2 u = *reinterpret_cast<const uint2 *>(p);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
+__device__ __forceinline__ void st4(__half *p, float4 v) {
+    __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<unsigned *>(&a);
+    u.y = *reinterpret_cast<unsigned *>(&b);
+    *reinterpret_cast<uint2 *>(p) = u;
+}
+__device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ float f4get(const float4 &v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// cluster plumbing (PTX)
+__device__ __forceinline__ void csync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_remote(uint32_t cluster_addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
+}
+
+// LAPACK dlarfg convention (scale-invariant, tau = 0 for a zero tail); same
+// scalar formula as the tree path's house_scalars (stage1_tree.cu).
+__device__ __forceinline__ void house(float alpha, float sig, float &beta, float &tau, float &scale) {
+    if (sig == 0.f) {
+        beta = alpha;
+        tau = 0.f;
+        scale = 0.f;   // v tail is zero either way
+    } else {
+        beta = -copysignf(__fsqrt_rn(fmaf(alpha, alpha, sig)), alpha);
+        const float d = alpha - beta;
+        scale = __frcp_rn(d);
+        tau = -d * __frcp_rn(beta);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Workspace of one matrix (floats):
+//   Vrm [n][TS] | Vcm[2][TS][n] (ping-pong: the next panel writes V while the
+//   previous side's k_fgemm2 still reads it) | tau[TS] | T[TS][TS] |
+//   Wp[nsplit][TS][n] | W2[TS][n] | Gp[kGSplit][TS][TS] | counter
+constexpr int kGSplit = 16;
+struct Ws {
+    float *Vrm, *Vcm0, *Vcm1, *tau, *T, *Wp, *W2, *Gp;
+    int *cnt;
+};
+__host__ __device__ inline size_t ws_floats(int64_t n, int ts, int nsplit) {
+    const size_t a = (size_t)n * ts * 3 + ts + (size_t)ts * ts + (size_t)nsplit * ts * n +
+                     (size_t)ts * n + (size_t)kGSplit * ts * ts + 64;
+    return (a + 63) & ~(size_t)63;
+}
+__host__ __device__ inline Ws ws_carve(float *base, int64_t n, int ts, int nsplit) {
+    Ws w;
+    w.Vrm = base;
+    w.Vcm0 = w.Vrm + (size_t)n * ts;
+    w.Vcm1 = w.Vcm0 + (size_t)n * ts;
+    w.tau = w.Vcm1 + (size_t)n * ts;
+    w.T = w.tau + ts;
+    w.Wp = w.T + (size_t)ts * ts;
+    w.W2 = w.Wp + (size_t)nsplit * ts * n;
+    w.Gp = w.W2 + (size_t)ts * n;
+    w.cnt = (int *)(w.Gp + (size_t)kGSplit * ts * ts);
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+// Panel.  One cluster of CS = gridDim.x CTAs per matrix (blockIdx.y = batch
+// member).  CTA c owns panel rows [c*RPC, (c+1)*RPC), RPC = 128*RPT; thread
+// (rg, q) -- rg = tid/4 in [0,128), q = tid%4 -- holds rows rg + 128 i
+// (i < RPT) x the 8 columns q*8..q*8+7 of the current 32-column sub-panel.
+template <int TS, int RPT>
+struct PanelSmem {
+    static constexpr int RPC = 128 * RPT;
+    static constexpr int VLD = 36;   // Vs row stride: conflict-free LDS.128 for (rg, q) lanes
+    static constexpr int WE = NB * (TS - NB > 0 ? TS - NB : 1);   // rest-block W elements
+    // Vs [RPC][VLD] | red8 [16][8][32] | Wc [WE] | W2s [WE] | RS [WE + kMaxCS]
+    static constexpr size_t floats = (size_t)RPC * VLD + 16 * 8 * 32 + 3 * WE + kMaxCS;
+    static constexpr size_t dyn = floats * 4;
+};
+
+template <typename S, int TS, int RPT>
+__global__ void __launch_bounds__(kPT, 1)
+k_fpanel(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, float *ws0,
+         int64_t ws_bstride, int64_t n, int nsplit, int par) {
+    using PS = PanelSmem<TS, RPT>;
+    constexpr int RPC = PS::RPC, VLD = PS::VLD;
+    __shared__ __align__(16) float red[16][32];
+    __shared__ __align__(16) float slots[2][kMaxCS][32];
+    __shared__ __align__(16) float prow_loc[32];
+    __shared__ __align__(16) float prow_slot[2][32];
+    __shared__ __align__(16) float fco[32];
+    __shared__ float scal[2];
+    __shared__ float Y[NB][NB + 1];
+    __shared__ float Ts[NB][NB + 1];
+    __shared__ float taus[NB];
+    extern __shared__ __align__(16) float dsm[];
+    float *Vs = dsm;                                  // [RPC][VLD]
+    float *red8 = dsm + (size_t)RPC * VLD;           // [16 warps][8][32]
+    float *Wc = red8 + 16 * 8 * 32;                  // [NB][Rc]
+    float *W2s = Wc + PS::WE;
+    float *RS = W2s + PS::WE;
+
+    const int b = blockIdx.y;
+    P += (int64_t)b * a_bstride;
+    Ws w = ws_carve(ws0 + (int64_t)b * ws_bstride, n, TS, nsplit);
+    float *Vcm = par ? w.Vcm1 : w.Vcm0;
+    const int CS = gridDim.x;
+    const int rank = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, rgw = lane >> 2, rg = warp * 8 + rgw;
+    const int rbase = rank * RPC + rg;   // row of i = 0
+    const unsigned FULL = 0xffffffffu;
+    const bool lqv = (cs == 1);          // columns contiguous in memory
+
+    auto elem = [&](int r, int c) -> S * { return P + (int64_t)r * rs + (int64_t)c * cs; };
+
+    // rows of the 8-column group q, cols [c0, c0+8), into x[8] (0 beyond M)
+    auto load8 = [&](int r, int c0, float (&x)[8]) {
+        if (r >= M) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = 0.f;
+            return;
+        }
+        if (lqv) {
+            const float4 u = ld4(elem(r, c0)), v = ld4(elem(r, c0 + 4));
+            x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
+            x[4] = v.x; x[5] = v.y; x[6] = v.z; x[7] = v.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = ldf(elem(r, c0 + c));
+        }
+    };
+
+    for (int s = 0; s < TS / NB; ++s) {
+        const int col0 = s * NB;
+        float a[RPT][8];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) load8(rbase + 128 * i, col0 + q * 8, a[i]);
+
+        // ---- 32 column steps, one cluster reduction each --------------------
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int jg = col0 + j;
+            const int qj = j >> 3, cj = j & 7;
+            const int pb = j & 1;
+            const int src = (lane & ~3) | qj;
+            float p[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) p[i] = __shfl_sync(FULL, a[i][cj], src);
+            float d[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) d[c] = 0.f;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const float pm = (rbase + 128 * i > jg) ? p[i] : 0.f;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) d[c] = fmaf(pm, a[i][c], d[c]);
+            }
+            // pivot row (row jg < TS <= RPC: CTA 0, i = 0, rg = jg)
+            if (rank == 0 && rg == jg) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) prow_loc[q * 8 + c] = a[0][c];
+            }
+            // reduce-scatter d over the 8 row groups of the warp (lane bits 2..4)
+            float e4[4], e2[2], dsum;
+            {
+                const bool hb = lane & 16;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float mine = hb ? d[4 + t] : d[t], oth = hb ? d[t] : d[4 + t];
+                    e4[t] = mine + __shfl_xor_sync(FULL, oth, 16);
+                }
+                const bool mb = lane & 8;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const float mine = mb ? e4[2 + t] : e4[t], oth = mb ? e4[t] : e4[2 + t];
+                    e2[t] = mine + __shfl_xor_sync(FULL, oth, 8);
+                }
+                const bool lb = lane & 4;
+                const float mine = lb ? e2[1] : e2[0], oth = lb ? e2[0] : e2[1];
+                dsum = mine + __shfl_xor_sync(FULL, oth, 4);
+            }
+            red[warp][q * 8 + rgw] = dsum;   // column q*8 + rgw
+            __syncthreads();
+            float g = 0.f;
+            if (warp == 0) {
+#pragma unroll
+                for (int ww = 0; ww < 16; ++ww) g += red[ww][lane];
+                if (CS > 1) {
+                    const uint32_t sa = smem_u32(&slots[pb][rank][lane]);
+                    const uint32_t pa = smem_u32(&prow_slot[pb][lane]);
+                    const float pr = prow_loc[lane];
+                    for (int t = 0; t < CS; ++t) {
+                        st_remote(mapa(sa, t), g);
+                        if (rank == 0) st_remote(mapa(pa, t), pr);
+                    }
+                }
+            }
+            if (CS > 1) csync();
+            if (warp == 0) {
+                float pr;
+                if (CS > 1) {
+                    g = 0.f;
+                    for (int t = 0; t < CS; ++t) g += slots[pb][t][lane];
+                    pr = prow_slot[pb][lane];
+                } else {
+                    pr = prow_loc[lane];
+                }
+                const float sigma = __shfl_sync(FULL, g, j), alpha = __shfl_sync(FULL, pr, j);
+                float beta, tau, scale;
+                house(alpha, sigma, beta, tau, scale);
+                const float wv = fmaf(g, scale, pr);   // v_j^T x_l (l > j) / v_l^T v_j (l < j)
+                fco[lane] = lane > j ? tau * wv : 0.f;
+                if (lane < j) Y[j][lane] = wv;
+                if (lane == 0) {
+                    scal[0] = scale;
+                    scal[1] = beta;
+                    taus[j] = tau;
+                }
+            }
+            __syncthreads();
+            const float scale = scal[0], beta = scal[1];
+            const float4 f0 = *reinterpret_cast<const float4 *>(&fco[q * 8]);
+            const float4 f1 = *reinterpret_cast<const float4 *>(&fco[q * 8 + 4]);
+            const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = rbase + 128 * i;
+                const float v = (r > jg) ? p[i] * scale : (r == jg ? 1.f : 0.f);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) a[i][c] = fmaf(-f[c], v, a[i][c]);
+                if (q == qj) a[i][cj] = (r > jg) ? v : (r == jg ? beta : a[i][cj]);
+            }
+        }
+
+        // ---- T of the sub-panel (forward larft from the V^T v columns) -----
+        if (warp == 0) {
+            if (lane < NB) Ts[lane][lane] = taus[lane];
+            __syncwarp();
+            for (int j = 1; j < NB; ++j) {
+                float t = 0.f;
+                if (lane < j)
+                    for (int c = lane; c < j; ++c) t = fmaf(Ts[lane][c], Y[j][c], t);
+                __syncwarp();
+                if (lane < j) Ts[lane][j] = -taus[j] * t;
+                __syncwarp();
+            }
+            if (rank == 0) w.tau[col0 + lane] = taus[lane];
+        }
+
+        // ---- write back: R / tails into the matrix, clean V to Vrm, Vcm, Vs --
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = rbase + 128 * i;
+            const int lr = rg + 128 * i;
+            float v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int cg = col0 + q * 8 + c;
+                v[c] = (r > cg) ? a[i][c] : (r == cg ? 1.f : 0.f);
+            }
+            *reinterpret_cast<float4 *>(&Vs[lr * VLD + q * 8]) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4 *>(&Vs[lr * VLD + q * 8 + 4]) = make_float4(v[4], v[5], v[6], v[7]);
+            if (r < M) {
+                if (lqv) {
+                    st4(elem(r, col0 + q * 8), make_float4(a[i][0], a[i][1], a[i][2], a[i][3]));
+                    st4(elem(r, col0 + q * 8 + 4), make_float4(a[i][4], a[i][5], a[i][6], a[i][7]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) stf(elem(r, col0 + q * 8 + c), a[i][c]);
+                }
+                float *vr = w.Vrm + (int64_t)r * TS + col0 + q * 8;
+                *reinterpret_cast<float4 *>(vr) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4 *>(vr + 4) = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) Vcm[(int64_t)(col0 + q * 8 + c) * M + r] = v[c];
+            }
+        }
+        __syncthreads();
+        if (s == TS / NB - 1) break;
+
+        // ---- block reflector of the sub-panel on the panel's rest columns ---
+        const int rc0 = col0 + NB;             // first rest column
+        const int Rc = TS - rc0;               // rest width (multiple of 32)
+        // W_cta = Vs^T A_rest over this CTA's rows, 8 rest columns per chunk
+        for (int cc = 0; cc < Rc / 8; ++cc) {
+            float acc[8][8];   // [c' (rest col in chunk)][c (V col in group q)]
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[x][c] = 0.f;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = rbase + 128 * i, lr = rg + 128 * i;
+                if (r < col0) continue;   // V rows above the sub-panel are zero
+                const float4 v0 = *reinterpret_cast<const float4 *>(&Vs[lr * VLD + q * 8]);
+                const float4 v1 = *reinterpret_cast<const float4 *>(&Vs[lr * VLD + q * 8 + 4]);
+                const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                float x[8];
+                load8(r, rc0 + cc * 8, x);
+#pragma unroll
+                for (int xx = 0; xx < 8; ++xx)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc[xx][c] = fmaf(v[c], x[xx], acc[xx][c]);
+            }
+            // reduce-scatter over the warp's 8 row groups: lane keeps c' = rgw
+            float h4[4][8], h2[2][8], h1[8];
+            {
+                const bool hb = lane & 16;
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float mine = hb ? acc[4 + t][c] : acc[t][c], oth = hb ? acc[t][c] : acc[4 + t][c];
+                        h4[t][c] = mine + __shfl_xor_sync(FULL, oth, 16);
+                    }
+                const bool mb = lane & 8;
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float mine = mb ? h4[2 + t][c] : h4[t][c], oth = mb ? h4[t][c] : h4[2 + t][c];
+                        h2[t][c] = mine + __shfl_xor_sync(FULL, oth, 8);
+                    }
+                const bool lb = lane & 4;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float mine = lb ? h2[1][c] : h2[0][c], oth = lb ? h2[0][c] : h2[1][c];
+                    h1[c] = mine + __shfl_xor_sync(FULL, oth, 4);
+                }
+            }
+            float *rb = red8 + (warp * 8 + rgw) * 32 + q * 8;   // [warp][c'][c]
+            *reinterpret_cast<float4 *>(rb) = make_float4(h1[0], h1[1], h1[2], h1[3]);
+            *reinterpret_cast<float4 *>(rb + 4) = make_float4(h1[4], h1[5], h1[6], h1[7]);
+            __syncthreads();
+            if (tid < 256) {
+                const int xx = tid >> 5, c = tid & 31;
+                float sum = 0.f;
+#pragma unroll
+                for (int ww = 0; ww < 16; ++ww) sum += red8[(ww * 8 + xx) * 32 + c];
+                Wc[c * Rc + cc * 8 + xx] = sum;   // Wc[c][c']
+            }
+            __syncthreads();
+        }
+        // cluster all-reduce of Wc (NB x Rc): reduce-scatter then all-gather
+        if (CS > 1) {
+            const int E = NB * Rc, slice = (E + CS - 1) / CS;
+            for (int e = tid; e < E; e += kPT) {
+                const int dst = e / slice, pos = e - dst * slice;
+                st_remote(mapa(smem_u32(&RS[rank * slice + pos]), dst), Wc[e]);
+            }
+            csync();
+            for (int pos = tid; pos < slice; pos += kPT) {
+                const int e = rank * slice + pos;
+                if (e < E) {
+                    float sum = 0.f;
+                    for (int t = 0; t < CS; ++t) sum += RS[t * slice + pos];
+                    const uint32_t la = smem_u32(&Wc[e]);
+                    for (int t = 0; t < CS; ++t) st_remote(mapa(la, t), sum);
+                }
+            }
+            csync();
+        }
+        // W2 = Ts^T Wc  (W2[c][x] = sum_{j<=c} Ts[j][c] Wc[j][x])
+        for (int e = tid; e < NB * Rc; e += kPT) {
+            const int c = e / Rc, x = e - c * Rc;
+            float sum = 0.f;
+            for (int j = 0; j <= c; ++j) sum = fmaf(Ts[j][c], Wc[j * Rc + x], sum);
+            W2s[e] = sum;
+        }
+        __syncthreads();
+        // A_rest -= Vs W2 (own rows): thread (rg, q) sums its 8 V columns, the
+        // 4 q lanes of a row reduce-scatter so lane q owns rest cols 2q, 2q+1
+        for (int cc = 0; cc < Rc / 8; ++cc) {
+            float wr[8][8];   // [c in group q][x in chunk]
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+#pragma unroll
+                for (int x = 0; x < 8; ++x) wr[c][x] = W2s[(q * 8 + c) * Rc + cc * 8 + x];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = rbase + 128 * i, lr = rg + 128 * i;
+                const float4 v0 = *reinterpret_cast<const float4 *>(&Vs[lr * VLD + q * 8]);
+                const float4 v1 = *reinterpret_cast<const float4 *>(&Vs[lr * VLD + q * 8 + 4]);
+                const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                float u[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    float t = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) t = fmaf(v[c], wr[c][x], t);
+                    u[x] = t;
+                }
+                // reduce-scatter over q (lane bits 0, 1)
+                float u4[4], u2[2];
+                const bool qb1 = lane & 2;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float mine = qb1 ? u[4 + t] : u[t], oth = qb1 ? u[t] : u[4 + t];
+                    u4[t] = mine + __shfl_xor_sync(FULL, oth, 2);
+                }
+                const bool qb0 = lane & 1;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const float mine = qb0 ? u4[2 + t] : u4[t], oth = qb0 ? u4[t] : u4[2 + t];
+                    u2[t] = mine + __shfl_xor_sync(FULL, oth, 1);
+                }
+                if (r < M && r >= col0) {
+                    const int x0 = rc0 + cc * 8 + q * 2;
+                    S *e0 = elem(r, x0), *e1 = elem(r, x0 + 1);
+                    stf(e0, ldf(e0) - u2[0]);
+                    stf(e1, ldf(e1) - u2[1]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// FMA GEMM core: C tile BM x BN, 256 threads, per-thread microtile TM x TN
+// (rows tm*4+{0..3} [+ BM/2 + ...], cols tn*4+{0..3} [+ BN/2 + ...]).
+// Operands staged in shared memory k-major: As[k][BM], Bs[k][BN+4].
+template <int BM, int BN>
+struct Tile {
+    static constexpr int TM = BM / 16, TN = BN / 16;
+    static constexpr int BNP = BN + 4;
+    static constexpr int A_EL = KC * BM, B_EL = KC * BNP;
+    __device__ static __forceinline__ int row(int tm, int ii) {
+        return (TM == 8) ? ((ii < 4) ? tm * 4 + ii : BM / 2 + tm * 4 + ii - 4) : tm * 4 + ii;
+    }
+    __device__ static __forceinline__ int col(int tn, int jj) {
+        return (TN == 8) ? ((jj < 4) ? tn * 4 + jj : BN / 2 + tn * 4 + jj - 4) : tn * 4 + jj;
+    }
+    // acc (+/-)= As^T Bs over one KC chunk
+    template <bool SUB>
+    __device__ static __forceinline__ void mma(const float *As, const float *Bs, float (&acc)[TM][TN],
+                                               int tm, int tn, int kmax = KC) {
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            if (k >= kmax) break;
+            float av[TM], bv[TN];
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[k * BM + tm * 4]);
+            av[0] = a0.x; av[1] = a0.y; av[2] = a0.z; av[3] = a0.w;
+            if (TM == 8) {
+                const float4 a1 = *reinterpret_cast<const float4 *>(&As[k * BM + BM / 2 + tm * 4]);
+                av[TM == 8 ? 4 : 0] = a1.x; av[TM == 8 ? 5 : 1] = a1.y;
+                av[TM == 8 ? 6 : 2] = a1.z; av[TM == 8 ? 7 : 3] = a1.w;
+            }
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[k * BNP + tn * 4]);
+            bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w;
+            if (TN == 8) {
+                const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[k * BNP + BN / 2 + tn * 4]);
+                bv[TN == 8 ? 4 : 0] = b1.x; bv[TN == 8 ? 5 : 1] = b1.y;
+                bv[TN == 8 ? 6 : 2] = b1.z; bv[TN == 8 ? 7 : 3] = b1.w;
+            }
+#pragma unroll
+            for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < TN; ++jj)
+                    acc[ii][jj] = SUB ? fmaf(-av[ii], bv[jj], acc[ii][jj]) : fmaf(av[ii], bv[jj], acc[ii][jj]);
+        }
+    }
+};
+
+// Chunk loaders: fetch one KC-chunk into registers, then commit to smem.
+// K-major source: element (k, m) at src[k*ld + m] (m contiguous), W columns.
+template <typename T, int W>
+struct LdKM {
+    static constexpr int PER = (KC * W / 4 + kGT - 1) / kGT;   // float4 per thread
+    float4 r[PER];
+    __device__ __forceinline__ void fetch(const T *src, int64_t ld, int k0, int kmax, int m0, int mmax) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            const int id = threadIdx.x + p * kGT;
+            const int k = id / (W / 4), m4 = (id % (W / 4)) * 4;
+            r[p] = f4zero();
+            if (id < KC * W / 4 && k0 + k < kmax && m0 + m4 < mmax) r[p] = ld4(src + (int64_t)(k0 + k) * ld + m0 + m4);
+        }
+    }
+    // sum of `cnt` equally strided sources (split-K partials), fixed order
+    __device__ __forceinline__ void fetch_sum(const float *src, int64_t ld, int64_t sstride, int cnt, int k0,
+                                              int kmax, int m0, int mmax) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            const int id = threadIdx.x + p * kGT;
+            const int k = id / (W / 4), m4 = (id % (W / 4)) * 4;
+            float4 acc = f4zero();
+            if (id < KC * W / 4 && k0 + k < kmax && m0 + m4 < mmax) {
+                const float *s0 = src + (int64_t)(k0 + k) * ld + m0 + m4;
+                for (int s = 0; s < cnt; ++s) {
+                    const float4 v = ld4(s0 + (int64_t)s * sstride);
+                    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                }
+            }
+            r[p] = acc;
+        }
+    }
+    __device__ __forceinline__ void commit(float *dst, int ldd) const {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            const int id = threadIdx.x + p * kGT;
+            if (id < KC * W / 4) {
+                const int k = id / (W / 4), m4 = (id % (W / 4)) * 4;
+                *reinterpret_cast<float4 *>(&dst[k * ldd + m4]) = r[p];
+            }
+        }
+    }
+};
+// M-major source (k contiguous): element (k, m) at src[m*ld + k]; transposed
+// into the k-major smem tile.
+template <typename T, int W>
+struct LdMK {
+    static constexpr int PER = (KC * W / 4 + kGT - 1) / kGT;
+    float4 r[PER];
+    __device__ __forceinline__ void fetch(const T *src, int64_t ld, int k0, int kmax, int m0, int mmax) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            const int id = threadIdx.x + p * kGT;
+            const int kq = id % (KC / 4), m = id / (KC / 4);
+            r[p] = f4zero();
+            if (id < KC * W / 4 && k0 + kq * 4 < kmax && m0 + m < mmax) r[p] = ld4(src + (int64_t)(m0 + m) * ld + k0 + kq * 4);
+        }
+    }
+    __device__ __forceinline__ void commit(float *dst, int ldd) const {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            const int id = threadIdx.x + p * kGT;
+            if (id < KC * W / 4) {
+                const int kq = id % (KC / 4), m = id / (KC / 4);
+                dst[(kq * 4 + 0) * ldd + m] = r[p].x;
+                dst[(kq * 4 + 1) * ldd + m] = r[p].y;
+                dst[(kq * 4 + 2) * ldd + m] = r[p].z;
+                dst[(kq * 4 + 3) * ldd + m] = r[p].w;
+            }
+        }
+    }
+};
+
+// C-tile I/O in the matrix view: element (r, c) at X[r*rs + c*cs]; one of rs,
+// cs is 1 (CM: rows contiguous, else columns contiguous).
+template <typename S, int BM, int BN, bool CM>
+__device__ __forceinline__ void tile_io(S *X, int64_t ld, int r0, int rmax, int c0, int cmax, int tm, int tn,
+                                        float (&acc)[BM / 16][BN / 16], bool store) {
+    using TL = Tile<BM, BN>;
+    constexpr int TM = TL::TM, TN = TL::TN;
+    if (CM) {   // rows contiguous: float4 along rows (r = row(tm, 4h..4h+3))
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) {
+            const int c = c0 + TL::col(tn, jj);
+            if (c >= cmax) continue;
+#pragma unroll
+            for (int h = 0; h < TM / 4; ++h) {
+                const int r = r0 + TL::row(tm, h * 4);
+                if (r >= rmax) continue;
+                S *p = X + (int64_t)c * ld + r;
+                if (store) {
+                    st4(p, make_float4(acc[h * 4][jj], acc[h * 4 + 1][jj], acc[h * 4 + 2][jj], acc[h * 4 + 3][jj]));
+                } else {
+                    const float4 v = ld4(p);
+                    acc[h * 4][jj] = v.x; acc[h * 4 + 1][jj] = v.y; acc[h * 4 + 2][jj] = v.z; acc[h * 4 + 3][jj] = v.w;
+                }
+            }
+        }
+    } else {    // columns contiguous
+#pragma unroll
+        for (int ii = 0; ii < TM; ++ii) {
+            const int r = r0 + TL::row(tm, ii);
+            if (r >= rmax) continue;
+#pragma unroll
+            for (int h = 0; h < TN / 4; ++h) {
+                const int c = c0 + TL::col(tn, h * 4);
+                if (c >= cmax) continue;
+                S *p = X + (int64_t)r * ld + c;
+                if (store) {
+                    st4(p, make_float4(acc[ii][h * 4], acc[ii][h * 4 + 1], acc[ii][h * 4 + 2], acc[ii][h * 4 + 3]));
+                } else {
+                    const float4 v = ld4(p);
+                    acc[ii][h * 4] = v.x; acc[ii][h * 4 + 1] = v.y; acc[ii][h * 4 + 2] = v.z; acc[ii][h * 4 + 3] = v.w;
+                }
+            }
+        }
+    }
+}
+
+// thread -> (tm, tn): the fast lane index runs along the contiguous axis of
+// the tile the kernel reads/writes in the matrix (coalesced 256-B rows)
+template <bool CM>
+__device__ __forceinline__ void tmtn(int &tm, int &tn) {
+    if (CM) { tm = threadIdx.x & 15; tn = threadIdx.x >> 4; }
+    else { tn = threadIdx.x & 15; tm = threadIdx.x >> 4; }
+}
+
+// ---------------------------------------------------------------------------
+// k_fgemm2: X[TS:M, :] -= V[TS:M, :] W2  (tile 128 x 128, K = TS).
+template <typename S, int TS, bool CM>
+__global__ void __launch_bounds__(kGT, 1)
+k_fgemm2(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, const float *ws0,
+         int64_t ws_bstride, int64_t n, int nsplit, int par) {
+    constexpr int BM = 128, BN = 128;
+    using TL = Tile<BM, BN>;
+    __shared__ __align__(16) float As[2][TL::A_EL];
+    __shared__ __align__(16) float Bs[2][TL::B_EL];
+    const int b = blockIdx.z;
+    X += (int64_t)b * a_bstride;
+    const Ws w = ws_carve(const_cast<float *>(ws0) + (int64_t)b * ws_bstride, n, TS, nsplit);
+    const float *Vcm = par ? w.Vcm1 : w.Vcm0;
+    const int r0 = TS + blockIdx.x * BM, c0 = blockIdx.y * BN;
+    int tm, tn;
+    tmtn<CM>(tm, tn);
+    float acc[TL::TM][TL::TN];
+    tile_io<S, BM, BN, CM>(X, ld, r0, M, c0, C, tm, tn, acc, false);
+    LdKM<float, BM> la;
+    LdKM<float, BN> lb;
+    la.fetch(Vcm, M, 0, TS, r0, M);
+    lb.fetch(w.W2, C, 0, TS, c0, C);
+    la.commit(As[0], BM);
+    lb.commit(Bs[0], TL::BNP);
+    __syncthreads();
+    constexpr int NCH = TS / KC;
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int cur = ch & 1;
+        if (ch + 1 < NCH) {
+            la.fetch(Vcm, M, (ch + 1) * KC, TS, r0, M);
+            lb.fetch(w.W2, C, (ch + 1) * KC, TS, c0, C);
+        }
+        TL::template mma<true>(As[cur], Bs[cur], acc, tm, tn);
+        if (ch + 1 < NCH) {
+            la.commit(As[cur ^ 1], BM);
+            lb.commit(Bs[cur ^ 1], TL::BNP);
+        }
+        __syncthreads();
+    }
+    tile_io<S, BM, BN, CM>(X, ld, r0, M, c0, C, tm, tn, acc, true);
+}
+
+// k_fgemm1: Wp[s] = V[rows_s]^T X[rows_s]  (tile TS x 128, K = rows of split s)
+template <typename S, int TS, bool CM>
+__global__ void __launch_bounds__(kGT, 1)
+k_fgemm1(const S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *ws0,
+         int64_t ws_bstride, int64_t n, int nsplit, int rps) {
+    constexpr int BM = TS, BN = 128;
+    using TL = Tile<BM, BN>;
+    __shared__ __align__(16) float As[2][TL::A_EL];
+    __shared__ __align__(16) float Bs[2][TL::B_EL];
+    const int b = blockIdx.z;
+    X += (int64_t)b * a_bstride;
+    const Ws w = ws_carve(ws0 + (int64_t)b * ws_bstride, n, TS, nsplit);
+    const int c0 = blockIdx.x * BN, sp = blockIdx.y;
+    const int k_lo = sp * rps, k_hi = min(M, k_lo + rps);
+    int tm, tn;
+    tmtn<false>(tm, tn);
+    float acc[TL::TM][TL::TN];
+#pragma unroll
+    for (int ii = 0; ii < TL::TM; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TL::TN; ++jj) acc[ii][jj] = 0.f;
+    LdKM<float, BM> la;
+    LdKM<S, BN> lbr;    // columns contiguous (LQ view)
+    LdMK<S, BN> lbc;    // rows contiguous (RQ view): transposed on commit
+    auto fetch = [&](int k0) {
+        la.fetch(w.Vrm, TS, k0, k_hi, 0, TS);
+        if (CM) lbc.fetch(X, ld, k0, k_hi, c0, C);
+        else lbr.fetch(X, ld, k0, k_hi, c0, C);
+    };
+    auto commit = [&](int buf) {
+        la.commit(As[buf], BM);
+        if (CM) lbc.commit(Bs[buf], TL::BNP);
+        else lbr.commit(Bs[buf], TL::BNP);
+    };
+    if (k_lo < k_hi) {
+        fetch(k_lo);
+        commit(0);
+        __syncthreads();
+        const int nch = (k_hi - k_lo + KC - 1) / KC;
+#pragma unroll 1
+        for (int ch = 0; ch < nch; ++ch) {
+            const int cur = ch & 1;
+            if (ch + 1 < nch) fetch(k_lo + (ch + 1) * KC);
+            TL::template mma<false>(As[cur], Bs[cur], acc, tm, tn);
+            if (ch + 1 < nch) commit(cur ^ 1);
+            __syncthreads();
+        }
+    }
+    float *Wp = w.Wp + (int64_t)sp * TS * C;
+    tile_io<float, BM, BN, false>(Wp, C, 0, TS, c0, C, tm, tn, acc, true);
+}
+
+// k_fw2x1: W2 = T^T sum_s Wp[s]  and  X[0:TS] -= V[0:TS] W2  (tile TS x 64)
+template <typename S, int TS, bool CM>
+__global__ void __launch_bounds__(kGT, 1)
+k_fw2x1(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *ws0, int64_t ws_bstride,
+        int64_t n, int nsplit, int nused, int par) {
+    constexpr int BM = TS, BN = 64;
+    using TL = Tile<BM, BN>;
+    __shared__ __align__(16) float As[2][TL::A_EL];
+    __shared__ __align__(16) float Bs[2][TL::B_EL];
+    extern __shared__ __align__(16) float W2s[];   // [TS][BNP]
+    const int b = blockIdx.z;
+    X += (int64_t)b * a_bstride;
+    const Ws w = ws_carve(ws0 + (int64_t)b * ws_bstride, n, TS, nsplit);
+    const float *Vcm = par ? w.Vcm1 : w.Vcm0;
+    const int c0 = blockIdx.x * BN;
+    int tm, tn;
+    tmtn<CM>(tm, tn);
+    float acc[TL::TM][TL::TN];
+#pragma unroll
+    for (int ii = 0; ii < TL::TM; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TL::TN; ++jj) acc[ii][jj] = 0.f;
+    // pass 1: W2 = T^T W  (A(k=j, m=i) = T(j, i): T stored row-major)
+    LdKM<float, BM> la;
+    LdKM<float, BN> lb;
+    constexpr int NCH = TS / KC;
+    la.fetch(w.T, TS, 0, TS, 0, TS);
+    lb.fetch_sum(w.Wp, C, (int64_t)TS * C, nused, 0, TS, c0, C);
+    la.commit(As[0], BM);
+    lb.commit(Bs[0], TL::BNP);
+    __syncthreads();
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int cur = ch & 1;
+        if (ch + 1 < NCH) {
+            la.fetch(w.T, TS, (ch + 1) * KC, TS, 0, TS);
+            lb.fetch_sum(w.Wp, C, (int64_t)TS * C, nused, (ch + 1) * KC, TS, c0, C);
+        }
+        TL::template mma<false>(As[cur], Bs[cur], acc, tm, tn);
+        if (ch + 1 < NCH) {
+            la.commit(As[cur ^ 1], BM);
+            lb.commit(Bs[cur ^ 1], TL::BNP);
+        }
+        __syncthreads();
+    }
+    // W2 -> global (for k_fgemm2) and smem (B operand of pass 2)
+#pragma unroll
+    for (int ii = 0; ii < TL::TM; ++ii) {
+        const int r = TL::row(tm, ii);
+#pragma unroll
+        for (int h = 0; h < TL::TN / 4; ++h) {
+            const int c = TL::col(tn, h * 4);
+            const float4 v = make_float4(acc[ii][h * 4], acc[ii][h * 4 + 1], acc[ii][h * 4 + 2], acc[ii][h * 4 + 3]);
+            *reinterpret_cast<float4 *>(&W2s[r * TL::BNP + c]) = v;
+            if (c0 + c < C) *reinterpret_cast<float4 *>(&w.W2[(int64_t)r * C + c0 + c]) = v;
+        }
+    }
+    // pass 2: X[0:TS] -= V[0:TS] W2
+    tile_io<S, BM, BN, CM>(X, ld, 0, TS, c0, C, tm, tn, acc, false);
+    la.fetch(Vcm, M, 0, TS, 0, TS);
+    la.commit(As[0], BM);
+    __syncthreads();
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int cur = ch & 1;
+        if (ch + 1 < NCH) la.fetch(Vcm, M, (ch + 1) * KC, TS, 0, TS);
+        TL::template mma<true>(As[cur], W2s + ch * KC * TL::BNP, acc, tm, tn);
+        if (ch + 1 < NCH) la.commit(As[cur ^ 1], BM);
+        __syncthreads();
+    }
+    tile_io<S, BM, BN, CM>(X, ld, 0, TS, c0, C, tm, tn, acc, true);
+}
+
+// k_fgram: G = V^T V over row splits; the last CTA merges the partials (fixed
+// order) and builds T (compact WY, forward) -> w.T row-major.
+template <int TS>
+__global__ void __launch_bounds__(kGT, 1)
+k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps) {
+    constexpr int BM = TS, BN = TS;
+    using TL = Tile<BM, BN>;
+    __shared__ __align__(16) float As[2][TL::A_EL];
+    __shared__ __align__(16) float Bs[2][TL::B_EL];
+    __shared__ int s_last;
+    extern __shared__ __align__(16) float Tsm[];   // [TS][TS+1] T, then tmp TS*TS/4
+    const int b = blockIdx.y;
+    const Ws w = ws_carve(ws0 + (int64_t)b * ws_bstride, n, TS, nsplit);
+    const int sp = blockIdx.x, ns = gridDim.x;
+    const int k_lo = sp * rps, k_hi = min(M, k_lo + rps);
+    int tm, tn;
+    tmtn<false>(tm, tn);
+    float acc[TL::TM][TL::TN];
+#pragma unroll
+    for (int ii = 0; ii < TL::TM; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TL::TN; ++jj) acc[ii][jj] = 0.f;
+    LdKM<float, BM> la;
+    LdKM<float, BN> lb;
+    if (k_lo < k_hi) {
+        la.fetch(w.Vrm, TS, k_lo, k_hi, 0, TS);
+        lb.fetch(w.Vrm, TS, k_lo, k_hi, 0, TS);
+        la.commit(As[0], BM);
+        lb.commit(Bs[0], TL::BNP);
+        __syncthreads();
+        const int nch = (k_hi - k_lo + KC - 1) / KC;
+#pragma unroll 1
+        for (int ch = 0; ch < nch; ++ch) {
+            const int cur = ch & 1;
+            if (ch + 1 < nch) {
+                la.fetch(w.Vrm, TS, k_lo + (ch + 1) * KC, k_hi, 0, TS);
+                lb.fetch(w.Vrm, TS, k_lo + (ch + 1) * KC, k_hi, 0, TS);
+            }
+            TL::template mma<false>(As[cur], Bs[cur], acc, tm, tn);
+            if (ch + 1 < nch) {
+                la.commit(As[cur ^ 1], BM);
+                lb.commit(Bs[cur ^ 1], TL::BNP);
+            }
+            __syncthreads();
+        }
+    }
+    float *Gp = w.Gp + (int64_t)sp * TS * TS;
+    tile_io<float, BM, BN, false>(Gp, TS, 0, TS, 0, TS, tm, tn, acc, true);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(w.cnt, 1) == ns - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    constexpr int LDT = TS + 1;
+    float *tmp = Tsm + TS * LDT;
+    for (int e = threadIdx.x; e < TS * TS; e += kGT) {
+        const int i = e / TS, j = e % TS;   // G(i, j), i < j kept (strict upper)
+        float sum = 0.f;
+        for (int s = 0; s < ns; ++s) sum += __ldcg(&w.Gp[(int64_t)s * TS * TS + e]);
+        Tsm[j * LDT + i] = (i < j) ? sum : 0.f;
+    }
+    __syncthreads();
+    panel::build_T_rec<float, TS, kGT>(w.tau, tmp, [&](int i, int j) -> float & { return Tsm[j * LDT + i]; });
+    __syncthreads();
+    for (int e = threadIdx.x; e < TS * TS; e += kGT) {
+        const int i = e / TS, jj = e % TS;   // w.T[i*TS + jj] = T(i, jj) (row-major), zero below
+        w.T[e] = (jj >= i) ? Tsm[jj * LDT + i] : 0.f;
+    }
+    if (threadIdx.x == 0) *w.cnt = 0;
+}
+
+__global__ void k_zero_cnt(float *ws0, int64_t ws_bstride, int64_t n, int ts, int nsplit, int64_t batch) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < batch) *ws_carve(ws0 + b * ws_bstride, n, ts, nsplit).cnt = 0;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct DevCtx {
+    cudaStream_t sp = nullptr, su = nullptr;
+    cudaEvent_t ev[6] = {};
+    bool attr_set = false;
+};
+static std::mutex g_mu;
+static DevCtx g_ctx[64];
+
+static cudaError_t dev_ctx(DevCtx *&out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx &c = g_ctx[dev & 63];
+    if (!c.sp) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if ((e = cudaStreamCreateWithPriority(&c.sp, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&c.su, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        for (auto &ev : c.ev)
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    out = &c;
+    return cudaSuccess;
+}
+
+static int pick_rpt(int m, int64_t batch) {
+    if (const char *s = getenv("BSVD_FLAT_RPT")) {
+        const int v = atoi(s);
+        if (v == 1 || v == 2 || v == 4 || v == 8) return (m + v - 1) / v <= kMaxCS ? v : 8;
+    }
+    if (batch > 1 && m <= 8) return m <= 1 ? 1 : (m <= 2 ? 2 : (m <= 4 ? 4 : 8));
+    if (m <= 4) return 1;
+    if (m <= 16) return 2;
+    if (m <= 64) return 4;
+    return 8;
+}
+
+static int nsplit_for(int64_t batch) { return batch >= 8 ? 1 : kMaxSplit; }
+
+template <typename S, int TS, int RPT>
+static cudaError_t launch_panel(S *P, int64_t rs, int64_t cs, int64_t a_bstride, int M, float *ws,
+                                int64_t ws_bstride, int64_t n, int nsplit, int par, int CS, int64_t batch,
+                                cudaStream_t st) {
+    auto kern = k_fpanel<S, TS, RPT>;
+    const size_t dyn = PanelSmem<TS, RPT>::dyn;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    if (CS > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+        return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)CS, (unsigned)batch, 1);
+    cfg.blockDim = dim3(kPT, 1, 1);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = CS > 1 ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kern, P, rs, cs, a_bstride, M, ws, ws_bstride, n, nsplit, par);
+    bsvd_host::count_launch();
+    return e;
+}
+
+template <typename S, int TS>
+static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, float *ws, cudaStream_t st,
+                            double *pms, double *tms, bool timed) {
+    DevCtx *cx = nullptr;
+    cudaError_t e = dev_ctx(cx);
+    if (e != cudaSuccess) return e;
+    const int64_t N = n / TS;
+    const int nsplit = nsplit_for(batch);
+    const int64_t wsb = (int64_t)ws_floats(n, TS, nsplit);
+    cudaStream_t sp = cx->sp, su = cx->su;
+    cudaEvent_t evStart = cx->ev[0], evP = cx->ev[1], ev1 = cx->ev[2], evW = cx->ev[3], evEndP = cx->ev[4],
+                evEndU = cx->ev[5];
+    {   // (function attributes are per device: set before every stage)
+        e = cudaFuncSetAttribute(k_fw2x1<S, TS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(TS * (64 + 4) * sizeof(float)));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_fw2x1<S, TS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(TS * (64 + 4) * sizeof(float)));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_fgram<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)((TS * (TS + 1) + TS * TS / 4) * sizeof(float)));
+        if (e != cudaSuccess) return e;
+    }
+    // the T-build arrival counter of every batch member starts at zero
+    k_zero_cnt<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, wsb, n, TS, nsplit, batch);
+    bsvd_host::count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    cudaEventRecord(evStart, st);
+    cudaStreamWaitEvent(sp, evStart, 0);
+    cudaStreamWaitEvent(su, evStart, 0);
+    cudaEvent_t tp0 = nullptr, tp1 = nullptr;
+    if (timed) {
+        cudaEventCreate(&tp0);
+        cudaEventCreate(&tp1);
+        cudaEventRecord(tp0, sp);
+    }
+    int par = 0;
+    auto side = [&](int64_t k, bool lq) -> cudaError_t {
+        const int64_t top = lq ? k + 1 : k;
+        if (top >= N) return cudaSuccess;
+        const int M = (int)((N - top) * TS);
+        const int C = (int)((N - 1 - k) * TS);
+        const int64_t rs = lq ? n : 1, cs = lq ? 1 : n;
+        S *P = a + top * TS * rs + k * TS * cs;
+        S *X = P + TS * cs;
+        const int m = (M + 127) / 128;
+        const int rpt = pick_rpt(m, batch);
+        const int CS = (m + rpt - 1) / rpt;
+        cudaError_t e2;
+        switch (rpt) {
+        case 1: e2 = launch_panel<S, TS, 1>(P, rs, cs, a_bstride, M, ws, wsb, n, nsplit, par, CS, batch, sp); break;
+        case 2: e2 = launch_panel<S, TS, 2>(P, rs, cs, a_bstride, M, ws, wsb, n, nsplit, par, CS, batch, sp); break;
+        case 4: e2 = launch_panel<S, TS, 4>(P, rs, cs, a_bstride, M, ws, wsb, n, nsplit, par, CS, batch, sp); break;
+        default: e2 = launch_panel<S, TS, 8>(P, rs, cs, a_bstride, M, ws, wsb, n, nsplit, par, CS, batch, sp); break;
+        }
+        if (e2 != cudaSuccess) return e2;
+        if (C > 0) {
+            cudaEventRecord(evP, sp);
+            // T from V^T V (overlaps the first product on the update stream)
+            const int gs = (int)std::min<int64_t>(kGSplit, std::max<int64_t>(1, M / 512));
+            const int grps = ((M + gs - 1) / gs + KC - 1) / KC * KC;
+            k_fgram<TS><<<dim3((unsigned)gs, (unsigned)batch), kGT, (TS * (TS + 1) + TS * TS / 4) * sizeof(float), sp>>>(
+                ws, wsb, n, nsplit, M, grps);
+            bsvd_host::count_launch();
+            if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            // W partials over row splits
+            const int cblk = (C + 127) / 128;
+            int ns = 1;
+            if (batch == 1) {
+                ns = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, (2 * 148 + cblk - 1) / cblk));
+                ns = std::min(ns, std::max(1, M / 256));
+            }
+            const int rps = ((M + ns - 1) / ns + KC - 1) / KC * KC;
+            cudaStreamWaitEvent(su, evP, 0);
+            if (lq)
+                k_fgemm1<S, TS, false><<<dim3((unsigned)cblk, (unsigned)ns, (unsigned)batch), kGT, 0, su>>>(
+                    X, rs, a_bstride, M, C, ws, wsb, n, nsplit, rps);
+            else
+                k_fgemm1<S, TS, true><<<dim3((unsigned)cblk, (unsigned)ns, (unsigned)batch), kGT, 0, su>>>(
+                    X, cs, a_bstride, M, C, ws, wsb, n, nsplit, rps);
+            bsvd_host::count_launch();
+            if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            cudaEventRecord(ev1, su);
+            cudaStreamWaitEvent(sp, ev1, 0);
+            const size_t w2sm = TS * (64 + 4) * sizeof(float);
+            if (lq)
+                k_fw2x1<S, TS, false><<<dim3((unsigned)((C + 63) / 64), 1, (unsigned)batch), kGT, w2sm, sp>>>(
+                    X, rs, a_bstride, M, C, ws, wsb, n, nsplit, ns, par);
+            else
+                k_fw2x1<S, TS, true><<<dim3((unsigned)((C + 63) / 64), 1, (unsigned)batch), kGT, w2sm, sp>>>(
+                    X, cs, a_bstride, M, C, ws, wsb, n, nsplit, ns, par);
+            bsvd_host::count_launch();
+            if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            if (M > TS) {
+                cudaEventRecord(evW, sp);
+                cudaStreamWaitEvent(su, evW, 0);
+                const dim3 g2((unsigned)((M - TS + 127) / 128), (unsigned)cblk, (unsigned)batch);
+                if (lq)
+                    k_fgemm2<S, TS, false><<<g2, kGT, 0, su>>>(X, rs, a_bstride, M, C, ws, wsb, n, nsplit, par);
+                else
+                    k_fgemm2<S, TS, true><<<g2, kGT, 0, su>>>(X, cs, a_bstride, M, C, ws, wsb, n, nsplit, par);
+                bsvd_host::count_launch();
+                if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            }
+        }
+        par ^= 1;
+        return cudaSuccess;
+    };
+    for (int64_t k = 0; k < N - 1 && e == cudaSuccess; ++k) {
+        if ((e = side(k, false)) != cudaSuccess) break;
+        e = side(k, true);
+    }
+    if (e == cudaSuccess) e = side(N - 1, false);
+    cudaEventRecord(evEndP, sp);
+    cudaEventRecord(evEndU, su);
+    cudaStreamWaitEvent(st, evEndP, 0);
+    cudaStreamWaitEvent(st, evEndU, 0);
+    if (timed) {
+        cudaEventRecord(tp1, st);
+        cudaEventSynchronize(tp1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tp0, tp1);
+        *pms += ms;   // the whole stage (panel chain and updates overlap)
+        *tms += ms;
+        cudaEventDestroy(tp0);
+        cudaEventDestroy(tp1);
+    }
+    return e;
+}
+
+}  // namespace flat
+
+size_t flat_workspace_bytes(int64_t n, int ts, int64_t batch) {
+    return flat::ws_floats(n, ts, flat::nsplit_for(batch)) * sizeof(float) * (size_t)batch;
+}
+
+bool flat_supported(int ts, int elem_bytes) {
+    if (const char *s = getenv("BSVD_FLAT")) {
+        if (atoi(s) == 0) return false;
+    }
+    return (ts == 64 || ts == 128) && elem_bytes <= 4;
+}
+
+template <typename S>
+cudaError_t banddiag_flat(S *a, int64_t n, int ts, int64_t batch, int64_t a_bstride, void *ws, cudaStream_t st,
+                          double *panel_ms, double *trail_ms) {
+    const bool timed = panel_ms != nullptr;
+    if (ts == 128) return flat::run_flat<S, 128>(a, n, batch, a_bstride, (float *)ws, st, panel_ms, trail_ms, timed);
+    return flat::run_flat<S, 64>(a, n, batch, a_bstride, (float *)ws, st, panel_ms, trail_ms, timed);
+}
+
+template cudaError_t banddiag_flat<float>(float *, int64_t, int, int64_t, int64_t, void *, cudaStream_t, double *, double *);
+template cudaError_t banddiag_flat<__half>(__half *, int64_t, int, int64_t, int64_t, void *, cudaStream_t, double *, double *);
+
+}  // namespace bsvd
