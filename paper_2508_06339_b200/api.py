@@ -12,8 +12,9 @@ Everything runs on the GPU through libbsvd.so (include/bsvd.h); there is no
 CPU fallback.  Host inputs (numpy / DenseMatrix) are copied to the device
 column-major exactly like ``DenseMatrix.from_array`` lays them out, results
 come back as numpy arrays in the compute dtype (FP16 -> float32), like the
-reference.  torch CUDA tensors are consumed in place (a row-major tensor is
-read as its transpose: sigma(A) = sigma(A^T)) and results stay on the device.
+reference.  torch CUDA tensors are consumed in place by ``svdvals`` (a row-major tensor
+is read as its transpose: sigma(A) = sigma(A^T)); the stage entry points copy
+a row-major tensor to column-major first.  Device results stay on the device.
 """
 from __future__ import annotations
 
@@ -50,10 +51,15 @@ def _torch_prec(t):
     return {torch.float64: FP64, torch.float32: FP32, torch.float16: FP16}.get(t.dtype)
 
 
-def _as_device_matrix(a, be: B200Backend):
-    """-> (tensor on device, precision, n, lda, is_host_input).
+def _as_device_matrix(a, be: B200Backend, transpose_ok: bool = True):
+    """-> (tensor on device, precision, n, lda, is_host_input, n_out).
 
-    The tensor's memory holds the matrix column-major with leading dim lda."""
+    The tensor's memory holds the matrix column-major with leading dim lda.
+    With ``transpose_ok`` (svdvals: sigma(A) = sigma(A^T)) a row-major torch
+    tensor is read in place as the column-major A^T; the stage entry points
+    (whose outputs are not transpose-invariant) get a real column-major copy.
+    ``n_out`` is the number of values the reference returns (``orig_n`` of a
+    padded DenseMatrix, secondstage.py:523,542)."""
     torch = _torch()
     if isinstance(a, torch.Tensor):
         if a.ndim != 2:
@@ -66,12 +72,13 @@ def _as_device_matrix(a, be: B200Backend):
             raise ShapeError(f"matrix must be square, got {a.shape[0]}x{a.shape[1]}")
         host = not a.is_cuda
         t = a.to(be.device) if host else a
-        if t.stride(1) == 1 and t.stride(0) >= t.shape[0]:
-            return t, prec, t.shape[0], t.stride(0), host       # read as A^T
-        if t.stride(0) == 1 and t.stride(1) >= t.shape[0]:
-            return t, prec, t.shape[0], t.stride(1), host       # column-major A
-        t = t.contiguous()
-        return t, prec, t.shape[0], t.shape[0], host
+        n = t.shape[0]
+        if t.stride(0) == 1 and t.stride(1) >= n:
+            return t, prec, n, t.stride(1), host, n       # column-major A
+        if transpose_ok and t.stride(1) == 1 and t.stride(0) >= n:
+            return t, prec, n, t.stride(0), host, n       # read as A^T
+        t = t.t().contiguous()                            # memory = column-major A
+        return t, prec, n, n, host, n
     # numpy / DenseMatrix (ours or the reference's): column-major storage copy
     if hasattr(a, "array") and hasattr(a, "precision") and not isinstance(a, np.ndarray):
         arr = np.asarray(a.array)
@@ -90,8 +97,8 @@ def _as_device_matrix(a, be: B200Backend):
         raise ShapeError("matrix must have size >= 1")
     f = np.asfortranarray(arr, dtype=prec.storage_dtype)
     t = torch.from_numpy(f.T).to(be.device, non_blocking=False)   # memory = column-major A
-    del n_orig
-    return t, prec, arr.shape[0], arr.shape[0], True
+    n_out = arr.shape[0] if n_orig is None else max(1, min(int(n_orig), arr.shape[0]))
+    return t, prec, arr.shape[0], arr.shape[0], True, n_out
 
 
 def _out_torch_dtype(prec):
@@ -122,7 +129,7 @@ def svdvals(a, cfg: KernelConfig | None = None, backend=None, timers=None):
     torch = _torch()
     be = _backend(backend)
     L = _lib.lib()
-    t, prec, n, lda, host = _as_device_matrix(a, be)
+    t, prec, n, lda, host, n_out = _as_device_matrix(a, be)
     if n < 1:
         raise ShapeError("matrix must have size >= 1")
     cfg = cfg if cfg is not None else KernelConfig.for_size(n)
@@ -134,12 +141,14 @@ def svdvals(a, cfg: KernelConfig | None = None, backend=None, timers=None):
     ws = be.workspace(nbytes)
     out = torch.empty(n, dtype=_out_torch_dtype(prec), device=be.device)
     tm = _prep_timers(timers)
-    with torch.cuda.device(be.device):
+    with torch.cuda.device(be.device), be.ordered(t, out, ws):
         _lib.check(L.bsvd_svdvals_ex(t.data_ptr(), prec.code, n, lda, ctypes.byref(ccfg),
                                      ctypes.byref(opt), out.data_ptr(), ws.data_ptr(), ws.numel(),
                                      be.stream_handle(), ctypes.byref(tm) if tm is not None else None))
     _add_timers(timers, tm)
     be.stats.launches += 1
+    if n_out < n:
+        out = out[:n_out]
     if host:
         return out.cpu().numpy()
     return out
@@ -173,7 +182,7 @@ def svdvals_batched(a, cfg: KernelConfig | None = None, backend=None, timers=Non
     ws = be.workspace(nbytes)
     out = torch.empty((B, n), dtype=_out_torch_dtype(prec), device=be.device)
     tm = _prep_timers(timers)
-    with torch.cuda.device(be.device):
+    with torch.cuda.device(be.device), be.ordered(t, out, ws):
         _lib.check(L.bsvd_svdvals_batched(t.data_ptr(), prec.code, n, n, n * n, B,
                                           ctypes.byref(ccfg), out.data_ptr(), ws.data_ptr(),
                                           ws.numel(), be.stream_handle(),
@@ -192,7 +201,7 @@ def banddiag(a, cfg: KernelConfig | None = None, backend=None):
     torch = _torch()
     be = _backend(backend)
     L = _lib.lib()
-    t, prec, n, lda, host = _as_device_matrix(a, be)
+    t, prec, n, lda, host, _ = _as_device_matrix(a, be, transpose_ok=False)
     cfg = cfg if cfg is not None else KernelConfig.for_size(n)
     ts = cfg.tilesize
     N = max(1, -(-n // ts))
@@ -207,7 +216,7 @@ def banddiag(a, cfg: KernelConfig | None = None, backend=None):
     opt.stage1_algo = be.stage1_algo
     nbytes = L.bsvd_workspace_bytes(prec.code, npad, 1, ctypes.byref(ccfg))
     ws = be.workspace(nbytes)
-    with torch.cuda.device(be.device):
+    with torch.cuda.device(be.device), be.ordered(work, ws):
         _lib.check(L.bsvd_banddiag(work.data_ptr(), prec.code, npad, ctypes.byref(ccfg),
                                    ctypes.byref(opt), ws.data_ptr(), ws.numel(), be.stream_handle()))
     if host:
@@ -222,14 +231,14 @@ def band_to_bidiagonal(band, bandwidth: int, backend=None):
     torch = _torch()
     be = _backend(backend)
     L = _lib.lib()
-    t, prec, n, lda, host = _as_device_matrix(band, be)
+    t, prec, n, lda, host, _ = _as_device_matrix(band, be, transpose_ok=False)
     t = torch.as_strided(t, (n, n), (lda, 1), t.storage_offset()).contiguous()
     d = torch.empty(n, dtype=torch.float64, device=be.device)
     e = torch.empty(max(n - 1, 1), dtype=torch.float64, device=be.device)
     if not 1 <= bandwidth <= 128:
         raise ConfigError(f"band width must lie in [1, 128], got {bandwidth}")
     ws = be.workspace(L.bsvd_band_workspace_bytes(n, int(bandwidth)))
-    with torch.cuda.device(be.device):
+    with torch.cuda.device(be.device), be.ordered(t, d, e, ws):
         _lib.check(L.bsvd_band_to_bidiagonal(t.data_ptr(), prec.code, n, int(bandwidth),
                                              d.data_ptr(), e.data_ptr(), ws.data_ptr(), ws.numel(),
                                              be.stream_handle()))
@@ -256,7 +265,7 @@ def bidiagonal_values(d, e, backend=None):
     if te.numel() == 0:
         te = torch.zeros(1, dtype=torch.float64, device=be.device)
     out = torch.empty(n, dtype=torch.float64, device=be.device)
-    with torch.cuda.device(be.device):
+    with torch.cuda.device(be.device), be.ordered(td, te, out):
         _lib.check(L.bsvd_bidiagonal_values(td.data_ptr(), te.data_ptr(), n, out.data_ptr(),
                                             be.stream_handle()))
     return out.cpu().numpy() if host else out

@@ -12,6 +12,7 @@ counterparts, so the reference's own driver (``bandsvd.banddiag`` /
 """
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -66,6 +67,30 @@ class B200Backend:
 
     def stream_handle(self) -> int:
         return int(self.cuda_stream().cuda_stream)
+
+    @contextlib.contextmanager
+    def ordered(self, *tensors):
+        """Order a library call on this backend's stream after the work the
+        caller's current stream queued (inputs, outputs, workspace), and the
+        caller's stream after the call; tensors touched on a foreign stream are
+        marked with record_stream so the caching allocator does not hand
+        their blocks out while the call may still use them."""
+        import torch
+        if self.stream is None:
+            yield
+            return
+        cur = torch.cuda.current_stream(self.device)
+        if self.stream == cur:
+            yield
+            return
+        self.stream.wait_stream(cur)
+        try:
+            yield
+        finally:
+            for t in tensors:
+                if t is not None and t.is_cuda:
+                    t.record_stream(self.stream)
+            cur.wait_stream(self.stream)
 
     def workspace(self, nbytes: int):
         """Cached device scratch (grown on demand; stream-ordered reuse)."""

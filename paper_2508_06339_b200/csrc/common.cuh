@@ -4,6 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "../../include/bsvd.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
@@ -11,6 +15,27 @@
 #endif
 
 namespace bsvd {
+
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device.  Function
+// attributes are per device (context), so the largest size set is remembered
+// per (kernel, device); thread-safe.
+inline cudaError_t ensure_smem_fn(const void *fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &have = done[{fn, dev}];
+    if (bytes <= have) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+template <typename F>
+inline cudaError_t ensure_smem(F *fn, size_t bytes) {
+    return ensure_smem_fn(reinterpret_cast<const void *>(fn), bytes);
+}
 
 // Storage <-> compute conversion.  FP16 is storage-only (precision.py:16-37):
 // loads widen exactly, stores round to nearest even like numpy's cast.

@@ -536,17 +536,10 @@ cudaError_t launch_apply_levels(S *a, int64_t n, int64_t batch, int64_t a_bstrid
     const int64_t cbase = (k + 1) * TS;
     const int64_t ts2x3 = 3 * (int64_t)TS * TS;
     const unsigned gx = (unsigned)((ncols + G::BN - 1) / G::BN);
-    static size_t set_leaf = 0, set_tt = 0;
     const size_t sl = apply_smem<C, TS>(false), stt = apply_smem<C, TS>(true);
     cudaError_t e;
-    if (sl > set_leaf) {
-        if ((e = cudaFuncSetAttribute(k_apply_leaf<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sl)) != cudaSuccess) return e;
-        set_leaf = sl;
-    }
-    if (stt > set_tt) {
-        if ((e = cudaFuncSetAttribute(k_apply_tt<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stt)) != cudaSuccess) return e;
-        set_tt = stt;
-    }
+    if ((e = ensure_smem(k_apply_leaf<S, C, TS>, sl)) != cudaSuccess) return e;
+    if ((e = ensure_smem(k_apply_tt<S, C, TS>, stt)) != cudaSuccess) return e;
     k_apply_leaf<S, C, TS><<<dim3(gx, (unsigned)m, (unsigned)batch), apply::kNT, sl, st>>>(
         V, top, cbase, ncols, nodes, ts2x3, ws_bstride, a_bstride);
     bsvd_host::count_launch();
@@ -583,36 +576,25 @@ cudaError_t launch_apply_level(S *a, int64_t n, int64_t batch, int64_t a_bstride
     const int64_t cbase = (k + 1) * TS;
     const int64_t ts2x3 = 3 * (int64_t)TS * TS;
     const unsigned gx = (unsigned)((ncols + G::BN - 1) / G::BN);
-    static size_t set_leaf = 0, set_tt = 0;
     const size_t sl = apply_smem<C, TS>(false), stt = apply_smem<C, TS>(true);
     cudaError_t e;
     const int lstride = ext ? 2 : 1;                    // m counts two-tile leaves
     if (j == 0 && ext) {
-        static size_t set2 = 0;
         const size_t s2 = apply_smem<C, TS>(true);
-        if (s2 > set2) {
-            if ((e = cudaFuncSetAttribute(k_apply_leaf2<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)) != cudaSuccess) return e;
-            set2 = s2;
-        }
+        if ((e = ensure_smem(k_apply_leaf2<S, C, TS>, s2)) != cudaSuccess) return e;
         k_apply_leaf2<S, C, TS><<<dim3(gx, (unsigned)m, (unsigned)batch), apply::kNT, s2, st>>>(
             V, top, mtiles, cbase, ncols, nodes, ext, ts2x3, ws_bstride, a_bstride);
         bsvd_host::count_launch();
         return cudaGetLastError();
     }
     if (j == 0) {
-        if (sl > set_leaf) {
-            if ((e = cudaFuncSetAttribute(k_apply_leaf<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sl)) != cudaSuccess) return e;
-            set_leaf = sl;
-        }
+        if ((e = ensure_smem(k_apply_leaf<S, C, TS>, sl)) != cudaSuccess) return e;
         k_apply_leaf<S, C, TS><<<dim3(gx, (unsigned)m, (unsigned)batch), apply::kNT, sl, st>>>(
             V, top, cbase, ncols, nodes, ts2x3, ws_bstride, a_bstride);
         bsvd_host::count_launch();
         return cudaGetLastError();
     }
-    if (stt > set_tt) {
-        if ((e = cudaFuncSetAttribute(k_apply_tt<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stt)) != cudaSuccess) return e;
-        set_tt = stt;
-    }
+    if ((e = ensure_smem(k_apply_tt<S, C, TS>, stt)) != cudaSuccess) return e;
     int64_t off = 0, cnt_prev = m;
     for (int q = 1; q < j; ++q) {
         off += cnt_prev;

@@ -338,13 +338,9 @@ cudaError_t launch_apply_level_tc(S *a, int64_t n, int64_t batch, int64_t a_bstr
     tcapply::View<S> V{a, lq ? n : 1, lq ? 1 : n};
     const int64_t cbase = (k + 1) * TS;
     const unsigned gx = (unsigned)(ncols / BN);
-    static bool set = false;
     cudaError_t e;
-    if (!set) {
-        if ((e = cudaFuncSetAttribute(k_apply_leaf_tc<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_apply_tt_tc<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)) != cudaSuccess) return e;
-        set = true;
-    }
+    if ((e = ensure_smem(k_apply_leaf_tc<S>, SMEM)) != cudaSuccess) return e;
+    if ((e = ensure_smem(k_apply_tt_tc<S>, SMEM)) != cudaSuccess) return e;
     if (j == 0) {
         k_apply_leaf_tc<S><<<dim3(gx, (unsigned)m, (unsigned)batch), NT, SMEM, st>>>(V, top, cbase, img,
                                                                                      img_bstride, a_bstride);

@@ -1137,14 +1137,10 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         bsvd_host::count_launch();
         return cudaGetLastError();
     };
-    static size_t set = 0;
-    if (psm > set) {
-        if ((err = cudaFuncSetAttribute(k_panel_leaf<S, C, TS, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
-        if ((err = cudaFuncSetAttribute(k_panel_tt<S, C, TS, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
-        if ((err = cudaFuncSetAttribute(k_panel_tt<S, C, TS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess) return err;
-        if (DEFER && (err = cudaFuncSetAttribute(k_node_tu<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NodeTU<C, TS>::smem)) != cudaSuccess) return err;
-        set = psm;
-    }
+    if ((err = ensure_smem(k_panel_leaf<S, C, TS, DEFER>, psm)) != cudaSuccess) return err;
+    if ((err = ensure_smem(k_panel_tt<S, C, TS, DEFER>, psm)) != cudaSuccess) return err;
+    if ((err = ensure_smem(k_panel_tt<S, C, TS, false>, psm)) != cudaSuccess) return err;
+    if (DEFER && (err = ensure_smem(k_node_tu<C, TS>, NodeTU<C, TS>::smem)) != cudaSuccess) return err;
     // second stream + events (per call; creation cost is microseconds)
     cudaStream_t caller = st, st2, st1 = nullptr;
     if ((err = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking)) != cudaSuccess) return err;
@@ -1187,14 +1183,10 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     if constexpr (Leaf2<C, TS>::ok && NodeTU2<C, TS>::smem <= 227 * 1024 && LeafU2<C, TS>::smem <= 227 * 1024)
         leaf2 = DEFER && !use_tc && !(getenv("BSVD_LEAF2") && atoi(getenv("BSVD_LEAF2")) == 0);
     if (leaf2) {
-        static bool set2 = false;
-        if (!set2) {
-            if ((err = cudaFuncSetAttribute(k_panel_leaf2<S, C, TS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Leaf2<C, TS>::smem)) != cudaSuccess) return err;
-            if ((err = cudaFuncSetAttribute(k_panel_leaf2<S, C, TS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Leaf2<C, TS>::smem)) != cudaSuccess) return err;
-            if ((err = cudaFuncSetAttribute(k_leaf2_u<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LeafU2<C, TS>::smem)) != cudaSuccess) return err;
-            if ((err = cudaFuncSetAttribute(k_node_tu2<C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NodeTU2<C, TS>::smem)) != cudaSuccess) return err;
-            set2 = true;
-        }
+        if ((err = ensure_smem(k_panel_leaf2<S, C, TS, true>, Leaf2<C, TS>::smem)) != cudaSuccess) return err;
+        if ((err = ensure_smem(k_panel_leaf2<S, C, TS, false>, Leaf2<C, TS>::smem)) != cudaSuccess) return err;
+        if ((err = ensure_smem(k_leaf2_u<C, TS>, LeafU2<C, TS>::smem)) != cudaSuccess) return err;
+        if ((err = ensure_smem(k_node_tu2<C, TS>, NodeTU2<C, TS>::smem)) != cudaSuccess) return err;
     }
     bool l2side = false;                                // the current side uses two-tile leaves
     int64_t mtiles = 0;                                 // its panel's tile rows
@@ -1640,20 +1632,12 @@ static cudaError_t run_tree(S *a, int64_t n, int64_t batch, int64_t a_bstride, v
     const size_t psm = TS >= 16 ? PanelBlk<C, TS>::smem : panel_smem<C, TS>();
     const size_t tsm = trail_smem<C, TS>(depth);
     if (tsm > 220 * 1024 || psm > 220 * 1024) return cudaErrorInvalidConfiguration;
-    static size_t psm_set = 0, tsm_set = 0;   // per instantiation
-    if (psm > psm_set) {
-        if constexpr (TS >= 16)
-            err = cudaFuncSetAttribute(k_panel_blk<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
-        else
-            err = cudaFuncSetAttribute(k_panel_tree<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
-        if (err != cudaSuccess) return err;
-        psm_set = psm;
-    }
-    if (tsm > tsm_set) {
-        err = cudaFuncSetAttribute(k_trail_tree<S, C, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-        if (err != cudaSuccess) return err;
-        tsm_set = tsm;
-    }
+    if constexpr (TS >= 16)
+        err = ensure_smem(k_panel_blk<S, C, TS>, psm);
+    else
+        err = ensure_smem(k_panel_tree<S, C, TS>, psm);
+    if (err != cudaSuccess) return err;
+    if ((err = ensure_smem(k_trail_tree<S, C, TS>, tsm)) != cudaSuccess) return err;
     constexpr int CB = TileCfg<C>::elems / TS;
     // Per-phase timing: three events per sweep side, recorded on the launch
     // stream and read once at the end (no per-side host sync).

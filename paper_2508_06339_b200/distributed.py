@@ -75,7 +75,11 @@ def svdvals_sharded(a=None, cfg=None, backend=None, group=None, *, batch: int | 
                                     cfg, backend)
             local = local if isinstance(local, torch.Tensor) else torch.from_numpy(local)
         else:
-            local = torch.zeros((0, n), dtype=torch.float32)
+            # same dtype as the other ranks' blocks (FP64 -> float64, else
+            # float32): all_gather needs equal element sizes on every rank
+            sdt = getattr(shard, "dtype", None)
+            f64 = sdt in (torch.float64, np.float64, np.dtype(np.float64))
+            local = torch.zeros((0, n), dtype=torch.float64 if f64 else torch.float32)
         if dist.get_backend(group) == "nccl":
             local = local.cuda()
     else:

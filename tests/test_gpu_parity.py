@@ -257,6 +257,7 @@ def test_leaf_full_t_paths(P, be_tree, oracle, monkeypatch, n, ft_min):
     """Two-tile leaves with full T from the panel + k_leaf2_u (FULLT, forced
     here for every side with BSVD_LEAF_FT_MIN=2; by default only panels of
     >= 32 tile rows) and the k_node_tu2 path agree with the oracle."""
+    monkeypatch.setenv("BSVD_FLAT", "0")          # the tree stage 1 these leaves belong to
     monkeypatch.setenv("BSVD_LEAF_FT_MIN", ft_min)
     a = np.random.default_rng(n).standard_normal((n, n)).astype(np.float32)
     got = P.svdvals(a, P.KernelConfig(tilesize=128), backend=be_tree)
@@ -276,3 +277,53 @@ def test_chase_edge_reload_modes(P, be_tree, oracle, monkeypatch, n, early):
     d, e = P.band_to_bidiagonal(a.astype(np.float32), 128, backend=be_tree)
     want = np.linalg.svd(a, compute_uv=False)
     assert_close(oracle.bidiagonal_values(d, e), want, np.float32, n, what=f"n={n} early={early}")
+
+
+# ---- boundary regressions (round-1 advisor findings) ----------------------
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_stage_entry_points_row_major_tensor(P, be_tree, oracle, dtype):
+    """band_to_bidiagonal / banddiag on a row-major torch CUDA tensor act on
+    the tensor's matrix, not on its transpose (a lower band would be read)."""
+    import torch
+    n, b = 300, 32
+    rng = np.random.default_rng(5)
+    a = np.triu(rng.standard_normal((n, n)))
+    a -= np.triu(a, b + 1)
+    a = a.astype(dtype)
+    t = torch.from_numpy(a).cuda()               # row-major, upper band
+    d, e = P.band_to_bidiagonal(t, b, backend=be_tree)
+    want = np.linalg.svd(a.astype(np.float64), compute_uv=False)
+    assert_close(oracle.bidiagonal_values(d.cpu().numpy(), e.cpu().numpy()), want, dtype, n,
+                 what="row-major band tensor")
+    full = rng.standard_normal((128, 128)).astype(dtype)
+    band_dev = P.banddiag(torch.from_numpy(full).cuda(), P.KernelConfig(tilesize=32), backend=be_tree)
+    band_host = P.banddiag(full, P.KernelConfig(tilesize=32), backend=be_tree)
+    # device result holds the band column-major (row-major storage of band^T)
+    assert np.allclose(band_dev.cpu().numpy().T, band_host, atol=1e-4 if dtype == np.float32 else 1e-12)
+
+
+def test_padded_dense_matrix_returns_orig_n(P, be_tree, oracle):
+    from paper_2508_06339_b200.matrix import DenseMatrix, pad_to_tiles
+    a = np.random.default_rng(6).standard_normal((100, 100)).astype(np.float32)
+    m = pad_to_tiles(DenseMatrix.from_array(a), 32)
+    assert m.rows == 128 and m.orig_n == 100
+    got = P.svdvals(m, P.KernelConfig(tilesize=32), backend=be_tree)
+    assert got.shape == (100,)
+    assert_close(got, oracle.svdvals(a, 32), np.float32, 100, what="padded DenseMatrix")
+
+
+def test_backend_on_side_stream(P, oracle):
+    """B200Backend(stream=s): inputs produced on the caller's stream are
+    consumed after they are ready and results are ordered before the caller
+    reads them."""
+    import torch
+    s = torch.cuda.Stream()
+    be = P.B200Backend(stream=s)
+    x = torch.randn(1024, 1024, device="cuda")
+    torch.cuda._sleep(20_000_000)               # keep the current stream busy
+    y = x * 2.0                                 # produced on the current stream
+    got = P.svdvals(y, P.KernelConfig(tilesize=64), backend=be)
+    vals = got.cpu().numpy()                    # read on the current stream
+    want = 2.0 * oracle.svdvals(x.cpu().numpy().T.copy(), 64)
+    assert_close(vals, want, np.float32, 1024, what="side stream")
