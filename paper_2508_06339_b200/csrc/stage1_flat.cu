@@ -497,6 +497,494 @@ k_fpanel(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, fl
 }
 
 // ---------------------------------------------------------------------------
+// Panel v2.  Same row/column mapping as k_fpanel, restructured for latency:
+//  * per column ONE __syncthreads: every warp sums the 16 warp partials of
+//    the column dots itself and forms the reflector redundantly (no serial
+//    single-warp phase and no second barrier); warp partials are double
+//    buffered by column parity;
+//  * the cluster exchange is one-way: warp 0 pushes its CTA's 32 partial dots
+//    (rank 0 also the pivot row) into every other CTA's slot with st.async,
+//    counted in bytes on the receiver's mbarrier (no cluster barrier, no L1
+//    flush); every CTA sums the slots in rank order, so all CTAs form
+//    bit-identical reflectors;
+//  * the 32 column steps run as 4 x 8 (only the 8 columns a thread holds are
+//    unrolled: the body stays in the instruction cache);
+//  * the sub-panel T is built row-parallel (lane i owns row i) while the
+//    other warps write the sub-panel back;
+//  * the rest of the panel streams through a 3-stage cp.async ring (no
+//    exposed load latency), V comes from registers, and the W = V^T A_rest
+//    all-reduce is a reduce-scatter + all-gather over st.async/mbarriers.
+// The panel's full T is NOT built here: k_fgemm1 forms G = V^T V as one more
+// column block and its last CTA builds T (off the panel chain).
+namespace p2 {
+__device__ __forceinline__ void mbar_init(uint64_t *m, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *m, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n\t}\n" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
+// 4-byte / 16-byte remote store into CTA `rank`'s shared memory, completion
+// counted on that CTA's mbarrier (same offset as `bar` locally)
+__device__ __forceinline__ void put1(const float *dst_local, uint64_t *bar_local, unsigned rank, float v) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                     mapa(smem_u32(dst_local), rank)),
+                 "r"(__float_as_uint(v)), "r"(mapa(smem_u32(bar_local), rank))
+                 : "memory");
+}
+__device__ __forceinline__ void put4(const float *dst_local, uint64_t *bar_local, unsigned rank, float4 v) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     mapa(smem_u32(dst_local), rank)),
+                 "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+                 "r"(__float_as_uint(v.w)), "r"(mapa(smem_u32(bar_local), rank))
+                 : "memory");
+}
+__device__ __forceinline__ void cp16(void *smem, const void *gmem, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Sum over the 8 lanes that differ in lane bits 2..4 (the warp's 8 row groups),
+// scattered: the lane with bits (h, m, l) keeps elements h*K/2 + m*K/4 + l*K/8 + t.
+template <int K>
+__device__ __forceinline__ void rs8(const float (&v)[K], float (&out)[K / 8], int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    float e1[K / 2], e2[K / 4];
+    const bool hb = lane & 16, mb = lane & 8, lb = lane & 4;
+#pragma unroll
+    for (int t = 0; t < K / 2; ++t) {
+        const float mine = hb ? v[K / 2 + t] : v[t], oth = hb ? v[t] : v[K / 2 + t];
+        e1[t] = mine + __shfl_xor_sync(FULL, oth, 16);
+    }
+#pragma unroll
+    for (int t = 0; t < K / 4; ++t) {
+        const float mine = mb ? e1[K / 4 + t] : e1[t], oth = mb ? e1[t] : e1[K / 4 + t];
+        e2[t] = mine + __shfl_xor_sync(FULL, oth, 8);
+    }
+#pragma unroll
+    for (int t = 0; t < K / 8; ++t) {
+        const float mine = lb ? e2[K / 8 + t] : e2[t], oth = lb ? e2[t] : e2[K / 8 + t];
+        out[t] = mine + __shfl_xor_sync(FULL, oth, 4);
+    }
+}
+}  // namespace p2
+
+template <typename S, int TS, int RPT>
+struct Panel2 {
+    static constexpr int RPC = 128 * RPT;
+    static constexpr int XW = (RPT >= 8 && sizeof(S) == 4) ? 4 : 8;   // rest columns per staged chunk
+    static constexpr int KV = XW * 8;                      // per-thread chunk partials
+    static constexpr int CHB = RPC * XW * (int)sizeof(S);  // bytes per staged chunk
+    static constexpr int CHF = (CHB + 15) / 16 * 4;        // in floats (16-B aligned)
+    static constexpr int NST = 3;
+    static constexpr int WE = NB * (TS - NB > 0 ? TS - NB : 1);
+    // ring [NST][CHF] | red8 [2][16][XW][32] | Wc [WE] | W2s [WE] | RS [WE + 4*kMaxCS]
+    static constexpr size_t floats = (size_t)NST * CHF + 2 * 16 * XW * 32 + 3 * (size_t)WE + 4 * kMaxCS;
+    static constexpr size_t dyn = floats * 4;
+};
+
+template <typename S, int TS, int RPT>
+__global__ void __launch_bounds__(kPT, 1)
+k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, float *ws0,
+          int64_t ws_bstride, int64_t n, int nsplit, int par) {
+    using PS = Panel2<S, TS, RPT>;
+    constexpr int RPC = PS::RPC, XW = PS::XW, KV = PS::KV;
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ __align__(16) float red[2][16][32];
+    __shared__ __align__(16) float slot[2][kMaxCS][32];
+    __shared__ __align__(16) float pslot[2][32];
+    __shared__ __align__(16) float prow[2][32];
+    __shared__ float Y[NB][NB + 1];
+    __shared__ __align__(16) float Ts[NB][NB + 1];
+    __shared__ float taus[NB];
+    __shared__ __align__(8) uint64_t mbar[4];   // [0,1] column exchange, [2] RS, [3] AG
+    extern __shared__ __align__(16) float dsm[];
+    float *ring = dsm;
+    float *red8 = ring + PS::NST * PS::CHF;        // [2][16][XW][32]
+    float *Wc = red8 + 2 * 16 * XW * 32;
+    float *W2s = Wc + PS::WE;
+    float *RS = W2s + PS::WE;
+
+    const int b = blockIdx.y;
+    P += (int64_t)b * a_bstride;
+    Ws w = ws_carve(ws0 + (int64_t)b * ws_bstride, n, TS, nsplit);
+    float *Vcm = par ? w.Vcm1 : w.Vcm0;
+    const int CS = gridDim.x;
+    const int rank = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, rgw = lane >> 2, rg = warp * 8 + rgw;
+    const int row0 = rank * RPC;
+    const int rbase = row0 + rg;
+    const bool lqv = (cs == 1);
+    auto elem = [&](int r, int c) -> S * { return P + (int64_t)r * rs + (int64_t)c * cs; };
+    auto load8 = [&](int r, int c0, float (&x)[8]) {
+        if (r >= M) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = 0.f;
+            return;
+        }
+        if (lqv) {
+            const float4 u = ld4(elem(r, c0)), v = ld4(elem(r, c0 + 4));
+            x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
+            x[4] = v.x; x[5] = v.y; x[6] = v.z; x[7] = v.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = ldf(elem(r, c0 + c));
+        }
+    };
+    if (CS > 1) {
+        if (tid == 0) {
+            for (int i = 0; i < 4; ++i) p2::mbar_init(&mbar[i], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        csync();
+    }
+    // bytes this CTA receives per column exchange: CS-1 partial-dot vectors
+    // (+ the pivot row from rank 0)
+    const unsigned col_bytes = (unsigned)(CS - 1) * 128u + (rank != 0 ? 128u : 0u);
+    int t_col = 0;    // column exchanges so far (buffer = t & 1, phase = (t >> 1) & 1)
+    int t_bnd = 0;    // boundary all-reduces so far
+
+    // stage XW rest columns [rc, rc + XW) of this CTA's rows into ring slot
+    auto stage = [&](int slot_i, int rc) {
+        S *dst = reinterpret_cast<S *>(ring + (size_t)slot_i * PS::CHF);
+        constexpr int EPV = 16 / (int)sizeof(S);
+        if (!lqv) {     // rows contiguous: [XW cols][RPC rows]
+            constexpr int SEGC = RPC / EPV;
+            for (int sg = tid; sg < XW * SEGC; sg += kPT) {
+                const int x = sg / SEGC, rr = (sg - x * SEGC) * EPV, r = row0 + rr;
+                const bool ok = r < M;
+                p2::cp16(dst + x * RPC + rr, ok ? elem(r, rc + x) : P, ok);
+            }
+        } else {        // columns contiguous: [RPC rows][XW cols]
+            constexpr int SPR = XW / EPV > 0 ? XW / EPV : 1;
+            for (int sg = tid; sg < RPC * SPR; sg += kPT) {
+                const int lr = sg / SPR, part = sg - lr * SPR, r = row0 + lr;
+                const bool ok = r < M;
+                p2::cp16(dst + lr * XW + part * EPV, ok ? elem(r, rc + part * EPV) : P, ok);
+            }
+        }
+        p2::cp_commit();
+    };
+    auto staged = [&](int slot_i, int lr, int x) -> float {
+        const S *src = reinterpret_cast<const S *>(ring + (size_t)slot_i * PS::CHF);
+        return lqv ? ldf(src + lr * XW + x) : ldf(src + x * RPC + lr);
+    };
+
+    float a[RPT][8];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) load8(rbase + 128 * i, q * 8, a[i]);
+
+    for (int s = 0; s < TS / NB; ++s) {
+        const int col0 = s * NB;
+        // ---- 32 column steps (4 x 8: only the thread's 8 columns unrolled) --
+#pragma unroll 1
+        for (int qj = 0; qj < 4; ++qj) {
+#pragma unroll
+            for (int cj = 0; cj < 8; ++cj) {
+                const int j = qj * 8 + cj, jg = col0 + j;
+                const int bf = t_col & 1;
+                const int src = (lane & ~3) | qj;
+                float p[RPT];
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) p[i] = __shfl_sync(FULL, a[i][cj], src);
+                float d[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) d[c] = 0.f;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const float pm = (rbase + 128 * i > jg) ? p[i] : 0.f;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) d[c] = fmaf(pm, a[i][c], d[c]);
+                }
+                if (rank == 0 && rg == jg) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) prow[bf][q * 8 + c] = a[0][c];
+                }
+                float dsum[1];
+                p2::rs8<8>(d, dsum, lane);
+                red[bf][warp][q * 8 + rgw] = dsum[0];
+                __syncthreads();
+                // every warp: the CTA's partial dot of column `lane`
+                float g = 0.f;
+#pragma unroll
+                for (int ww = 0; ww < 16; ++ww) g += red[bf][ww][lane];
+                float pr;
+                if (CS > 1) {
+                    if (warp == 0) {
+                        if (lane == 0) p2::mbar_expect(&mbar[bf], col_bytes);
+                        for (int t = 0; t < CS; ++t) {
+                            if (t == rank) continue;
+                            p2::put1(&slot[bf][rank][lane], &mbar[bf], (unsigned)t, g);
+                            if (rank == 0) p2::put1(&pslot[bf][lane], &mbar[bf], (unsigned)t, prow[bf][lane]);
+                        }
+                    }
+                    p2::mbar_wait(&mbar[bf], (unsigned)((t_col >> 1) & 1));
+                    float gs = 0.f;
+                    for (int t = 0; t < CS; ++t) gs += (t == rank) ? g : slot[bf][t][lane];
+                    g = gs;
+                    pr = rank == 0 ? prow[bf][lane] : pslot[bf][lane];
+                } else {
+                    pr = prow[bf][lane];
+                }
+                ++t_col;
+                const float sigma = __shfl_sync(FULL, g, j), alpha = __shfl_sync(FULL, pr, j);
+                float beta, tau, scale;
+                house(alpha, sigma, beta, tau, scale);
+                const float wv = fmaf(g, scale, pr);   // v_j^T x_l (l > j) / v_l^T v_j (l < j)
+                const float fco = lane > j ? tau * wv : 0.f;
+                if (warp == 0) {
+                    if (lane < j) Y[j][lane] = wv;
+                    if (lane == 0) taus[j] = tau;
+                }
+                float f[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) f[c] = __shfl_sync(FULL, fco, q * 8 + c);
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int r = rbase + 128 * i;
+                    const float v = (r > jg) ? p[i] * scale : (r == jg ? 1.f : 0.f);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) a[i][c] = fmaf(-f[c], v, a[i][c]);
+                    if (q == qj) a[i][cj] = (r > jg) ? v : (r == jg ? beta : a[i][cj]);
+                }
+            }
+        }
+        __syncthreads();   // Y, taus complete
+
+        // ---- write back R / tails, clean V -> Vrm, Vcm; T_s by warp 0 -------
+        if (warp == 0) {
+            float tr[NB];
+            const int i = lane;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                for (int c = 0; c < j; ++c) {
+                    const float y = Y[j][c];
+                    if (c & 1) s1 = (c >= i) ? fmaf(tr[c], y, s1) : s1;
+                    else s0 = (c >= i) ? fmaf(tr[c], y, s0) : s0;
+                }
+                tr[j] = (j < i) ? 0.f : (j == i ? taus[j] : -taus[j] * (s0 + s1));
+            }
+#pragma unroll
+            for (int j = 0; j < NB; ++j) Ts[i][j] = tr[j];
+            if (rank == 0) w.tau[col0 + lane] = taus[lane];
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = rbase + 128 * i;
+            float v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int cg = col0 + q * 8 + c;
+                v[c] = (r > cg) ? a[i][c] : (r == cg ? 1.f : 0.f);
+            }
+            if (r < M) {
+                if (lqv) {
+                    st4(elem(r, col0 + q * 8), make_float4(a[i][0], a[i][1], a[i][2], a[i][3]));
+                    st4(elem(r, col0 + q * 8 + 4), make_float4(a[i][4], a[i][5], a[i][6], a[i][7]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) stf(elem(r, col0 + q * 8 + c), a[i][c]);
+                }
+                float *vr = w.Vrm + (int64_t)r * TS + col0 + q * 8;
+                *reinterpret_cast<float4 *>(vr) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4 *>(vr + 4) = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) Vcm[(int64_t)(col0 + q * 8 + c) * M + r] = v[c];
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) a[i][c] = v[c];   // a := clean V from here on
+        }
+        if (s == TS / NB - 1) break;
+
+        // ---- block reflector of the sub-panel on the rest of the panel -------
+        const int rc0 = col0 + NB, Rc = TS - rc0;
+        const int nch = Rc / XW;
+        stage(0, rc0);
+        if (nch > 1) stage(1, rc0 + XW);
+        // W_cta[c][x] = sum over own rows of V(r, c) A(r, rc0 + x)
+#pragma unroll 1
+        for (int cc = 0; cc <= nch; ++cc) {
+            if (cc < nch) {
+                if (cc + 1 < nch) p2::cp_wait<1>();
+                else p2::cp_wait<0>();
+            }
+            __syncthreads();   // chunk cc landed (all threads' copies); red8[(cc-1)&1] complete
+            if (cc + 2 < nch) stage((cc + 2) % PS::NST, rc0 + (cc + 2) * XW);
+            if (cc > 0 && tid < XW * 32) {       // fold chunk cc-1 over the 16 warps
+                const float *rb = red8 + ((cc - 1) & 1) * 16 * XW * 32;
+                const int xx = tid >> 5, c = tid & 31;
+                float sum = 0.f;
+#pragma unroll
+                for (int ww = 0; ww < 16; ++ww) sum += rb[(ww * XW + xx) * 32 + c];
+                Wc[c * Rc + (cc - 1) * XW + xx] = sum;
+            }
+            if (cc == nch) break;
+            float acc[KV];   // [xx][c]
+#pragma unroll
+            for (int e = 0; e < KV; ++e) acc[e] = 0.f;
+            const int sl = cc % PS::NST;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int lr = rg + 128 * i;
+                if (row0 + lr < col0) continue;   // V rows above the sub-panel are zero
+                float x[XW];
+#pragma unroll
+                for (int xx = 0; xx < XW; ++xx) x[xx] = staged(sl, lr, xx);
+#pragma unroll
+                for (int xx = 0; xx < XW; ++xx)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc[xx * 8 + c] = fmaf(a[i][c], x[xx], acc[xx * 8 + c]);
+            }
+            float h[KV / 8];
+            p2::rs8<KV>(acc, h, lane);
+            // lane keeps idx = rgw' * (KV/8) + t  ->  (xx, c) = divmod(idx, 8)
+            float *rb = red8 + (cc & 1) * 16 * XW * 32;
+#pragma unroll
+            for (int t = 0; t < KV / 8; ++t) {
+                const int idx = rgw * (KV / 8) + t, xx = idx >> 3, c = idx & 7;
+                rb[(warp * XW + xx) * 32 + q * 8 + c] = h[t];
+            }
+        }
+        __syncthreads();   // Wc complete (the last chunk's fold)
+        // cluster all-reduce of Wc (NB x Rc): reduce-scatter + all-gather
+        if (CS > 1) {
+            const int E = NB * Rc;
+            const int slice = ((E + CS - 1) / CS + 3) & ~3;
+            const int own_lo = rank * slice, own_len = max(0, min(slice, E - own_lo));
+            const unsigned ph = (unsigned)(t_bnd & 1);
+            if (tid == 0) {
+                p2::mbar_expect(&mbar[2], (unsigned)((CS - 1) * own_len * 4));
+                p2::mbar_expect(&mbar[3], (unsigned)((E - own_len) * 4));
+            }
+            for (int e4 = tid * 4; e4 < E; e4 += kPT * 4) {
+                const int dst = e4 / slice;
+                if (dst == rank) continue;
+                const float4 v = *reinterpret_cast<const float4 *>(&Wc[e4]);
+                p2::put4(&RS[rank * slice + (e4 - dst * slice)], &mbar[2], (unsigned)dst, v);
+            }
+            p2::mbar_wait(&mbar[2], ph);
+            for (int p4 = tid * 4; p4 < own_len; p4 += kPT * 4) {
+                float4 sum = f4zero();
+                for (int t = 0; t < CS; ++t) {
+                    const float4 v = (t == rank) ? *reinterpret_cast<const float4 *>(&Wc[own_lo + p4])
+                                                 : *reinterpret_cast<const float4 *>(&RS[t * slice + p4]);
+                    sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+                }
+                *reinterpret_cast<float4 *>(&Wc[own_lo + p4]) = sum;
+                for (int t = 0; t < CS; ++t)
+                    if (t != rank) p2::put4(&Wc[own_lo + p4], &mbar[3], (unsigned)t, sum);
+            }
+            p2::mbar_wait(&mbar[3], ph);
+            ++t_bnd;
+            __syncthreads();   // own slice (local stores) visible
+        }
+        // W2 = Ts^T Wc  (W2[c][x] = sum_{j<=c} Ts[j][c] Wc[j][x])
+        for (int e = tid; e < NB * Rc; e += kPT) {
+            const int c = e / Rc, x = e - c * Rc;
+            float s0 = 0.f, s1 = 0.f;
+            int j = 0;
+            for (; j + 1 <= c; j += 2) {
+                s0 = fmaf(Ts[j][c], Wc[j * Rc + x], s0);
+                s1 = fmaf(Ts[j + 1][c], Wc[(j + 1) * Rc + x], s1);
+            }
+            if (j <= c) s0 = fmaf(Ts[j][c], Wc[j * Rc + x], s0);
+            W2s[e] = s0 + s1;
+        }
+        __syncthreads();
+        // A_rest -= V W2 (own rows): the 4 q lanes of a row reduce-scatter so
+        // lane q owns rest columns 2q, 2q+1 of each 8-column chunk
+        {
+            auto ld2 = [&](int r, int x0, float &u0, float &u1) {
+                if (r >= M || r < col0) { u0 = u1 = 0.f; return; }
+                if (lqv && sizeof(S) == 4) {
+                    const float2 t = *reinterpret_cast<const float2 *>(elem(r, x0));
+                    u0 = t.x; u1 = t.y;
+                } else {
+                    u0 = ldf(elem(r, x0));
+                    u1 = ldf(elem(r, x0 + 1));
+                }
+            };
+            float cur[RPT][2], nxt[RPT][2];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) ld2(rbase + 128 * i, rc0 + q * 2, cur[i][0], cur[i][1]);
+#pragma unroll 1
+            for (int cc = 0; cc < Rc / 8; ++cc) {
+                if (cc + 1 < Rc / 8) {
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) ld2(rbase + 128 * i, rc0 + (cc + 1) * 8 + q * 2, nxt[i][0], nxt[i][1]);
+                }
+                float wr[8][8];   // [c in group q][x in chunk]
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float4 w0 = *reinterpret_cast<const float4 *>(&W2s[(q * 8 + c) * Rc + cc * 8]);
+                    const float4 w1 = *reinterpret_cast<const float4 *>(&W2s[(q * 8 + c) * Rc + cc * 8 + 4]);
+                    wr[c][0] = w0.x; wr[c][1] = w0.y; wr[c][2] = w0.z; wr[c][3] = w0.w;
+                    wr[c][4] = w1.x; wr[c][5] = w1.y; wr[c][6] = w1.z; wr[c][7] = w1.w;
+                }
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int r = rbase + 128 * i;
+                    float u[8];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        float t = 0.f;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) t = fmaf(a[i][c], wr[c][x], t);
+                        u[x] = t;
+                    }
+                    float u4[4], u2[2];
+                    const bool qb1 = lane & 2, qb0 = lane & 1;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float mine = qb1 ? u[4 + t] : u[t], oth = qb1 ? u[t] : u[4 + t];
+                        u4[t] = mine + __shfl_xor_sync(FULL, oth, 2);
+                    }
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const float mine = qb0 ? u4[2 + t] : u4[t], oth = qb0 ? u4[t] : u4[2 + t];
+                        u2[t] = mine + __shfl_xor_sync(FULL, oth, 1);
+                    }
+                    if (r < M && r >= col0) {
+                        const int x0 = rc0 + cc * 8 + q * 2;
+                        const float o0 = cur[i][0] - u2[0], o1 = cur[i][1] - u2[1];
+                        if (lqv && sizeof(S) == 4) {
+                            *reinterpret_cast<float2 *>(elem(r, x0)) = make_float2(o0, o1);
+                        } else {
+                            stf(elem(r, x0), o0);
+                            stf(elem(r, x0 + 1), o1);
+                        }
+                    }
+                }
+                if (cc + 1 < Rc / 8) {
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) { cur[i][0] = nxt[i][0]; cur[i][1] = nxt[i][1]; }
+                }
+            }
+        }
+        __syncthreads();   // updated rest columns visible to the next sub-panel's loads
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) load8(rbase + 128 * i, rc0 + q * 8, a[i]);
+    }
+    if (CS > 1) csync();   // no CTA exits while cluster peers may still address it
+}
+
+// ---------------------------------------------------------------------------
 // FMA GEMM core: C tile BM x BN, 256 threads, per-thread microtile TM x TN
 // (rows tm*4+{0..3} [+ BM/2 + ...], cols tn*4+{0..3} [+ BN/2 + ...]).
 // Operands staged in shared memory k-major: As[k][BM], Bs[k][BN+4].
@@ -963,8 +1451,9 @@ template <typename S, int TS, int RPT>
 static cudaError_t launch_panel(S *P, int64_t rs, int64_t cs, int64_t a_bstride, int M, float *ws,
                                 int64_t ws_bstride, int64_t n, int nsplit, int par, int CS, int64_t batch,
                                 cudaStream_t st) {
-    auto kern = k_fpanel<S, TS, RPT>;
-    const size_t dyn = PanelSmem<TS, RPT>::dyn;
+    static const bool v1 = getenv("BSVD_FPANEL_V1") && atoi(getenv("BSVD_FPANEL_V1")) != 0;
+    auto kern = v1 ? k_fpanel<S, TS, RPT> : k_fpanel2<S, TS, RPT>;
+    const size_t dyn = v1 ? PanelSmem<TS, RPT>::dyn : Panel2<S, TS, RPT>::dyn;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
     if (CS > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
