@@ -517,6 +517,15 @@ k_fpanel(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, fl
 // The panel's full T is NOT built here: k_fgemm1 forms G = V^T V as one more
 // column block and its last CTA builds T (off the panel chain).
 namespace p2 {
+// development instrumentation (BSVD_FPANEL_TRACE): phase timestamps of CTA 0
+__device__ unsigned long long *g_trace = nullptr;
+__device__ __forceinline__ void stamp(int i) {
+    if (g_trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[i] = t;
+    }
+}
 __device__ __forceinline__ void mbar_init(uint64_t *m, unsigned cnt) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(cnt) : "memory");
 }
@@ -591,8 +600,9 @@ struct Panel2 {
     static constexpr int CHF = (CHB + 15) / 16 * 4;        // in floats (16-B aligned)
     static constexpr int NST = 3;
     static constexpr int WE = NB * (TS - NB > 0 ? TS - NB : 1);
-    // ring [NST][CHF] | red8 [2][16][XW][32] | Wc [WE] | W2s [WE] | RS [WE + 4*kMaxCS]
-    static constexpr size_t floats = (size_t)NST * CHF + 2 * 16 * XW * 32 + 3 * (size_t)WE + 4 * kMaxCS;
+    static constexpr int R8 = 16 * XW * 33;               // red8 buffer (row stride 33)
+    // ring [NST][CHF] | red8 [2][R8] | Wc [WE] (x-major [x][32]) | W2 [WE] ([x][32]) | RS [WE + 4*kMaxCS]
+    static constexpr size_t floats = (size_t)NST * CHF + 2 * R8 + 3 * (size_t)WE + 4 * kMaxCS;
     static constexpr size_t dyn = floats * 4;
 };
 
@@ -613,8 +623,8 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
     __shared__ __align__(8) uint64_t mbar[4];   // [0,1] column exchange, [2] RS, [3] AG
     extern __shared__ __align__(16) float dsm[];
     float *ring = dsm;
-    float *red8 = ring + PS::NST * PS::CHF;        // [2][16][XW][32]
-    float *Wc = red8 + 2 * 16 * XW * 32;
+    float *red8 = ring + PS::NST * PS::CHF;        // [2][16][XW][33]
+    float *Wc = red8 + 2 * PS::R8;
     float *W2s = Wc + PS::WE;
     float *RS = W2s + PS::WE;
 
@@ -688,11 +698,13 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
 #pragma unroll
     for (int i = 0; i < RPT; ++i) load8(rbase + 128 * i, q * 8, a[i]);
 
+    p2::stamp(0);
     for (int s = 0; s < TS / NB; ++s) {
         const int col0 = s * NB;
         // ---- 32 column steps (4 x 8: only the thread's 8 columns unrolled) --
 #pragma unroll 1
         for (int qj = 0; qj < 4; ++qj) {
+            p2::stamp(1 + s * 12 + qj);
 #pragma unroll
             for (int cj = 0; cj < 8; ++cj) {
                 const int j = qj * 8 + cj, jg = col0 + j;
@@ -718,24 +730,38 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
                 p2::rs8<8>(d, dsum, lane);
                 red[bf][warp][q * 8 + rgw] = dsum[0];
                 __syncthreads();
-                // every warp: the CTA's partial dot of column `lane`
-                float g = 0.f;
+                // every warp: the CTA's partial dot of column `lane` (fixed tree)
+                float g;
+                {
+                    float v[16];
 #pragma unroll
-                for (int ww = 0; ww < 16; ++ww) g += red[bf][ww][lane];
+                    for (int ww = 0; ww < 16; ++ww) v[ww] = red[bf][ww][lane];
+#pragma unroll
+                    for (int h = 8; h > 0; h >>= 1)
+#pragma unroll
+                        for (int u = 0; u < h; ++u) v[u] += v[u + h];
+                    g = v[0];
+                }
                 float pr;
                 if (CS > 1) {
-                    if (warp == 0) {
-                        if (lane == 0) p2::mbar_expect(&mbar[bf], col_bytes);
-                        for (int t = 0; t < CS; ++t) {
-                            if (t == rank) continue;
-                            p2::put1(&slot[bf][rank][lane], &mbar[bf], (unsigned)t, g);
-                            if (rank == 0) p2::put1(&pslot[bf][lane], &mbar[bf], (unsigned)t, prow[bf][lane]);
-                        }
+                    // warp t pushes to CTA t (every warp holds g): the sends of
+                    // one column leave in parallel, not 15 deep from one warp
+                    if (warp == 0 && lane == 0) p2::mbar_expect(&mbar[bf], col_bytes);
+                    if (warp < CS && warp != rank) {
+                        p2::put1(&slot[bf][rank][lane], &mbar[bf], (unsigned)warp, g);
+                        if (rank == 0) p2::put1(&pslot[bf][lane], &mbar[bf], (unsigned)warp, prow[bf][lane]);
                     }
                     p2::mbar_wait(&mbar[bf], (unsigned)((t_col >> 1) & 1));
-                    float gs = 0.f;
-                    for (int t = 0; t < CS; ++t) gs += (t == rank) ? g : slot[bf][t][lane];
-                    g = gs;
+                    // same tree on every CTA (own term from registers): identical sums
+                    float v[kMaxCS];
+#pragma unroll
+                    for (int t = 0; t < kMaxCS; ++t)
+                        v[t] = t < CS ? (t == rank ? g : slot[bf][t][lane]) : 0.f;
+#pragma unroll
+                    for (int h = kMaxCS / 2; h > 0; h >>= 1)
+#pragma unroll
+                        for (int u = 0; u < h; ++u) v[u] += v[u + h];
+                    g = v[0];
                     pr = rank == 0 ? prow[bf][lane] : pslot[bf][lane];
                 } else {
                     pr = prow[bf][lane];
@@ -764,6 +790,7 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
             }
         }
         __syncthreads();   // Y, taus complete
+        p2::stamp(1 + s * 12 + 4);
 
         // ---- write back R / tails, clean V -> Vrm, Vcm; T_s by warp 0 -------
         if (warp == 0) {
@@ -794,12 +821,17 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
                 v[c] = (r > cg) ? a[i][c] : (r == cg ? 1.f : 0.f);
             }
             if (r < M) {
-                if (lqv) {
-                    st4(elem(r, col0 + q * 8), make_float4(a[i][0], a[i][1], a[i][2], a[i][3]));
-                    st4(elem(r, col0 + q * 8 + 4), make_float4(a[i][4], a[i][5], a[i][6], a[i][7]));
-                } else {
+                // only the top TS rows (R) are band: the V tails below them lie
+                // outside the band and are never read again (the band packer
+                // reads rows [c - b, c]; banddiag clears outside the band)
+                if (r < TS) {
+                    if (lqv) {
+                        st4(elem(r, col0 + q * 8), make_float4(a[i][0], a[i][1], a[i][2], a[i][3]));
+                        st4(elem(r, col0 + q * 8 + 4), make_float4(a[i][4], a[i][5], a[i][6], a[i][7]));
+                    } else {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) stf(elem(r, col0 + q * 8 + c), a[i][c]);
+                        for (int c = 0; c < 8; ++c) stf(elem(r, col0 + q * 8 + c), a[i][c]);
+                    }
                 }
                 float *vr = w.Vrm + (int64_t)r * TS + col0 + q * 8;
                 *reinterpret_cast<float4 *>(vr) = make_float4(v[0], v[1], v[2], v[3]);
@@ -810,6 +842,7 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
 #pragma unroll
             for (int c = 0; c < 8; ++c) a[i][c] = v[c];   // a := clean V from here on
         }
+        p2::stamp(1 + s * 12 + 5);
         if (s == TS / NB - 1) break;
 
         // ---- block reflector of the sub-panel on the rest of the panel -------
@@ -827,12 +860,16 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
             __syncthreads();   // chunk cc landed (all threads' copies); red8[(cc-1)&1] complete
             if (cc + 2 < nch) stage((cc + 2) % PS::NST, rc0 + (cc + 2) * XW);
             if (cc > 0 && tid < XW * 32) {       // fold chunk cc-1 over the 16 warps
-                const float *rb = red8 + ((cc - 1) & 1) * 16 * XW * 32;
+                const float *rb = red8 + ((cc - 1) & 1) * PS::R8;
                 const int xx = tid >> 5, c = tid & 31;
-                float sum = 0.f;
+                float v[16];
 #pragma unroll
-                for (int ww = 0; ww < 16; ++ww) sum += rb[(ww * XW + xx) * 32 + c];
-                Wc[c * Rc + (cc - 1) * XW + xx] = sum;
+                for (int ww = 0; ww < 16; ++ww) v[ww] = rb[(ww * XW + xx) * 33 + c];
+#pragma unroll
+                for (int h = 8; h > 0; h >>= 1)
+#pragma unroll
+                    for (int u = 0; u < h; ++u) v[u] += v[u + h];
+                Wc[((cc - 1) * XW + xx) * 32 + c] = v[0];
             }
             if (cc == nch) break;
             float acc[KV];   // [xx][c]
@@ -844,8 +881,17 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
                 const int lr = rg + 128 * i;
                 if (row0 + lr < col0) continue;   // V rows above the sub-panel are zero
                 float x[XW];
+                if (lqv && sizeof(S) == 4) {
+                    const float *src = ring + (size_t)sl * PS::CHF + lr * XW;
 #pragma unroll
-                for (int xx = 0; xx < XW; ++xx) x[xx] = staged(sl, lr, xx);
+                    for (int x4 = 0; x4 < XW; x4 += 4) {
+                        const float4 t = *reinterpret_cast<const float4 *>(src + x4);
+                        x[x4] = t.x; x[x4 + 1] = t.y; x[x4 + 2] = t.z; x[x4 + 3] = t.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int xx = 0; xx < XW; ++xx) x[xx] = staged(sl, lr, xx);
+                }
 #pragma unroll
                 for (int xx = 0; xx < XW; ++xx)
 #pragma unroll
@@ -854,14 +900,15 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
             float h[KV / 8];
             p2::rs8<KV>(acc, h, lane);
             // lane keeps idx = rgw' * (KV/8) + t  ->  (xx, c) = divmod(idx, 8)
-            float *rb = red8 + (cc & 1) * 16 * XW * 32;
+            float *rb = red8 + (cc & 1) * PS::R8;
 #pragma unroll
             for (int t = 0; t < KV / 8; ++t) {
                 const int idx = rgw * (KV / 8) + t, xx = idx >> 3, c = idx & 7;
-                rb[(warp * XW + xx) * 32 + q * 8 + c] = h[t];
+                rb[(warp * XW + xx) * 33 + q * 8 + c] = h[t];
             }
         }
         __syncthreads();   // Wc complete (the last chunk's fold)
+        p2::stamp(1 + s * 12 + 6);
         // cluster all-reduce of Wc (NB x Rc): reduce-scatter + all-gather
         if (CS > 1) {
             const int E = NB * Rc;
@@ -894,17 +941,20 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
             ++t_bnd;
             __syncthreads();   // own slice (local stores) visible
         }
-        // W2 = Ts^T Wc  (W2[c][x] = sum_{j<=c} Ts[j][c] Wc[j][x])
+        p2::stamp(1 + s * 12 + 7);
+        // W2 = Ts^T Wc  (W2[x][c] = sum_{j<=c} Ts[j][c] Wc[x][j]); lanes run over c
         for (int e = tid; e < NB * Rc; e += kPT) {
-            const int c = e / Rc, x = e - c * Rc;
-            float s0 = 0.f, s1 = 0.f;
-            int j = 0;
-            for (; j + 1 <= c; j += 2) {
-                s0 = fmaf(Ts[j][c], Wc[j * Rc + x], s0);
-                s1 = fmaf(Ts[j + 1][c], Wc[(j + 1) * Rc + x], s1);
+            const int x = e >> 5, c = e & 31;
+            const float *wx = Wc + x * 32;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int j = 0; j < NB; j += 4) {
+                if (j <= c) s0 = fmaf(Ts[j][c], wx[j], s0);
+                if (j + 1 <= c) s1 = fmaf(Ts[j + 1][c], wx[j + 1], s1);
+                if (j + 2 <= c) s2 = fmaf(Ts[j + 2][c], wx[j + 2], s2);
+                if (j + 3 <= c) s3 = fmaf(Ts[j + 3][c], wx[j + 3], s3);
             }
-            if (j <= c) s0 = fmaf(Ts[j][c], Wc[j * Rc + x], s0);
-            W2s[e] = s0 + s1;
+            W2s[e] = (s0 + s1) + (s2 + s3);
         }
         __syncthreads();
         // A_rest -= V W2 (own rows): the 4 q lanes of a row reduce-scatter so
@@ -931,11 +981,11 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
                 }
                 float wr[8][8];   // [c in group q][x in chunk]
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float4 w0 = *reinterpret_cast<const float4 *>(&W2s[(q * 8 + c) * Rc + cc * 8]);
-                    const float4 w1 = *reinterpret_cast<const float4 *>(&W2s[(q * 8 + c) * Rc + cc * 8 + 4]);
-                    wr[c][0] = w0.x; wr[c][1] = w0.y; wr[c][2] = w0.z; wr[c][3] = w0.w;
-                    wr[c][4] = w1.x; wr[c][5] = w1.y; wr[c][6] = w1.z; wr[c][7] = w1.w;
+                for (int x = 0; x < 8; ++x) {
+                    const float4 w0 = *reinterpret_cast<const float4 *>(&W2s[(cc * 8 + x) * 32 + q * 8]);
+                    const float4 w1 = *reinterpret_cast<const float4 *>(&W2s[(cc * 8 + x) * 32 + q * 8 + 4]);
+                    wr[0][x] = w0.x; wr[1][x] = w0.y; wr[2][x] = w0.z; wr[3][x] = w0.w;
+                    wr[4][x] = w1.x; wr[5][x] = w1.y; wr[6][x] = w1.z; wr[7][x] = w1.w;
                 }
 #pragma unroll
                 for (int i = 0; i < RPT; ++i) {
@@ -978,9 +1028,11 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
             }
         }
         __syncthreads();   // updated rest columns visible to the next sub-panel's loads
+        p2::stamp(1 + s * 12 + 8);
 #pragma unroll
         for (int i = 0; i < RPT; ++i) load8(rbase + 128 * i, rc0 + q * 8, a[i]);
     }
+    p2::stamp(60);
     if (CS > 1) csync();   // no CTA exits while cluster peers may still address it
 }
 
@@ -1512,6 +1564,14 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         cudaEventRecord(tp0, sp);
     }
     int par = 0;
+    const char *trace_path = getenv("BSVD_FPANEL_TRACE");
+    const int trace_side = getenv("BSVD_FPANEL_TRACE_SIDE") ? atoi(getenv("BSVD_FPANEL_TRACE_SIDE")) : 0;
+    unsigned long long *trace_buf = nullptr;
+    int side_no = 0;
+    if (trace_path) {
+        cudaMalloc(&trace_buf, 64 * 8);
+        cudaMemset(trace_buf, 0, 64 * 8);
+    }
     auto side = [&](int64_t k, bool lq) -> cudaError_t {
         const int64_t top = lq ? k + 1 : k;
         if (top >= N) return cudaSuccess;
@@ -1524,6 +1584,8 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         const int rpt = pick_rpt(m, batch);
         const int CS = (m + rpt - 1) / rpt;
         cudaError_t e2;
+        const bool tr_this = trace_buf && side_no++ == trace_side;
+        if (tr_this) cudaMemcpyToSymbolAsync(p2::g_trace, &trace_buf, sizeof(void *), 0, cudaMemcpyHostToDevice, sp);
         switch (rpt) {
         case 1: e2 = launch_panel<S, TS, 1>(P, rs, cs, a_bstride, M, ws, wsb, n, nsplit, par, CS, batch, sp); break;
         case 2: e2 = launch_panel<S, TS, 2>(P, rs, cs, a_bstride, M, ws, wsb, n, nsplit, par, CS, batch, sp); break;
@@ -1531,6 +1593,19 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         default: e2 = launch_panel<S, TS, 8>(P, rs, cs, a_bstride, M, ws, wsb, n, nsplit, par, CS, batch, sp); break;
         }
         if (e2 != cudaSuccess) return e2;
+        if (tr_this) {
+            void *null_ptr = nullptr;
+            cudaMemcpyToSymbolAsync(p2::g_trace, &null_ptr, sizeof(void *), 0, cudaMemcpyHostToDevice, sp);
+            unsigned long long h[64];
+            cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, sp);
+            cudaStreamSynchronize(sp);
+            if (FILE *f = fopen(trace_path, "w")) {
+                fprintf(f, "side %d M %d CS %d RPT %d\n", trace_side, M, CS, rpt);
+                for (int i = 0; i < 64; ++i)
+                    if (h[i]) fprintf(f, "%d %.3f\n", i, (double)(h[i] - h[0]) * 1e-3);
+                fclose(f);
+            }
+        }
         if (C > 0) {
             cudaEventRecord(evP, sp);
             // T from V^T V (overlaps the first product on the update stream)
@@ -1602,6 +1677,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         cudaEventDestroy(tp0);
         cudaEventDestroy(tp1);
     }
+    if (trace_buf) cudaFree(trace_buf);
     return e;
 }
 
