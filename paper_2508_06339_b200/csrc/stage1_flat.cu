@@ -115,29 +115,32 @@ __device__ __forceinline__ void house(float alpha, float sig, float &beta, float
 
 // ---------------------------------------------------------------------------
 // Workspace of one matrix (floats):
-//   Vrm [n][TS] | Vcm[2][TS][n] (ping-pong: the next panel writes V while the
+//   Vrm[2][n][TS] | Vcm[2][TS][n] (leading dim n; ping-pong: the next panel writes V while the
 //   previous side's k_fgemm2 still reads it) | tau[TS] | T[TS][TS] |
 //   Wp[nsplit][TS][n] | W2[TS][n] | Gp[kGSplit][TS][TS] | counter
 constexpr int kGSplit = 16;
 struct Ws {
-    float *Vrm, *Vcm0, *Vcm1, *tau, *T, *Wp, *W2, *Gp;
+    float *Vrm0, *Vrm1, *Vcm0, *Vcm1, *tau, *T, *Wp, *W2, *W2T, *Gp;
+    __host__ __device__ float *vrm(int par) const { return par ? Vrm1 : Vrm0; }
     int *cnt;
 };
 __host__ __device__ inline size_t ws_floats(int64_t n, int ts, int nsplit) {
-    const size_t a = (size_t)n * ts * 3 + ts + (size_t)ts * ts + (size_t)nsplit * ts * n +
-                     (size_t)ts * n + (size_t)kGSplit * ts * ts + 64;
+    const size_t a = (size_t)n * ts * 4 + ts + (size_t)ts * ts + (size_t)nsplit * ts * n +
+                     2 * (size_t)ts * n + (size_t)kGSplit * ts * ts + 64;
     return (a + 63) & ~(size_t)63;
 }
 __host__ __device__ inline Ws ws_carve(float *base, int64_t n, int ts, int nsplit) {
     Ws w;
-    w.Vrm = base;
-    w.Vcm0 = w.Vrm + (size_t)n * ts;
+    w.Vrm0 = base;
+    w.Vrm1 = w.Vrm0 + (size_t)n * ts;
+    w.Vcm0 = w.Vrm1 + (size_t)n * ts;
     w.Vcm1 = w.Vcm0 + (size_t)n * ts;
     w.tau = w.Vcm1 + (size_t)n * ts;
     w.T = w.tau + ts;
     w.Wp = w.T + (size_t)ts * ts;
     w.W2 = w.Wp + (size_t)nsplit * ts * n;
-    w.Gp = w.W2 + (size_t)ts * n;
+    w.W2T = w.W2 + (size_t)ts * n;
+    w.Gp = w.W2T + (size_t)ts * n;
     w.cnt = (int *)(w.Gp + (size_t)kGSplit * ts * ts);
     return w;
 }
@@ -348,11 +351,11 @@ k_fpanel(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, fl
 #pragma unroll
                     for (int c = 0; c < 8; ++c) stf(elem(r, col0 + q * 8 + c), a[i][c]);
                 }
-                float *vr = w.Vrm + (int64_t)r * TS + col0 + q * 8;
+                float *vr = w.vrm(par) + (int64_t)r * TS + col0 + q * 8;
                 *reinterpret_cast<float4 *>(vr) = make_float4(v[0], v[1], v[2], v[3]);
                 *reinterpret_cast<float4 *>(vr + 4) = make_float4(v[4], v[5], v[6], v[7]);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) Vcm[(int64_t)(col0 + q * 8 + c) * M + r] = v[c];
+                for (int c = 0; c < 8; ++c) Vcm[(int64_t)(col0 + q * 8 + c) * n + r] = v[c];
             }
         }
         __syncthreads();
@@ -833,11 +836,11 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
                         for (int c = 0; c < 8; ++c) stf(elem(r, col0 + q * 8 + c), a[i][c]);
                     }
                 }
-                float *vr = w.Vrm + (int64_t)r * TS + col0 + q * 8;
+                float *vr = w.vrm(par) + (int64_t)r * TS + col0 + q * 8;
                 *reinterpret_cast<float4 *>(vr) = make_float4(v[0], v[1], v[2], v[3]);
                 *reinterpret_cast<float4 *>(vr + 4) = make_float4(v[4], v[5], v[6], v[7]);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) Vcm[(int64_t)(col0 + q * 8 + c) * M + r] = v[c];
+                for (int c = 0; c < 8; ++c) Vcm[(int64_t)(col0 + q * 8 + c) * n + r] = v[c];
             }
 #pragma unroll
             for (int c = 0; c < 8; ++c) a[i][c] = v[c];   // a := clean V from here on
@@ -1231,7 +1234,7 @@ k_fgemm2(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, const f
     tile_io<S, BM, BN, CM>(X, ld, r0, M, c0, C, tm, tn, acc, false);
     LdKM<float, BM> la;
     LdKM<float, BN> lb;
-    la.fetch(Vcm, M, 0, TS, r0, M);
+    la.fetch(Vcm, n, 0, TS, r0, M);
     lb.fetch(w.W2, C, 0, TS, c0, C);
     la.commit(As[0], BM);
     lb.commit(Bs[0], TL::BNP);
@@ -1241,7 +1244,7 @@ k_fgemm2(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, const f
     for (int ch = 0; ch < NCH; ++ch) {
         const int cur = ch & 1;
         if (ch + 1 < NCH) {
-            la.fetch(Vcm, M, (ch + 1) * KC, TS, r0, M);
+            la.fetch(Vcm, n, (ch + 1) * KC, TS, r0, M);
             lb.fetch(w.W2, C, (ch + 1) * KC, TS, c0, C);
         }
         TL::template mma<true>(As[cur], Bs[cur], acc, tm, tn);
@@ -1258,7 +1261,7 @@ k_fgemm2(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, const f
 template <typename S, int TS, bool CM>
 __global__ void __launch_bounds__(kGT, 1)
 k_fgemm1(const S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *ws0,
-         int64_t ws_bstride, int64_t n, int nsplit, int rps) {
+         int64_t ws_bstride, int64_t n, int nsplit, int rps, int par) {
     constexpr int BM = TS, BN = 128;
     using TL = Tile<BM, BN>;
     __shared__ __align__(16) float As[2][TL::A_EL];
@@ -1279,7 +1282,7 @@ k_fgemm1(const S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, f
     LdKM<S, BN> lbr;    // columns contiguous (LQ view)
     LdMK<S, BN> lbc;    // rows contiguous (RQ view): transposed on commit
     auto fetch = [&](int k0) {
-        la.fetch(w.Vrm, TS, k0, k_hi, 0, TS);
+        la.fetch(w.vrm(par), TS, k0, k_hi, 0, TS);
         if (CM) lbc.fetch(X, ld, k0, k_hi, c0, C);
         else lbr.fetch(X, ld, k0, k_hi, c0, C);
     };
@@ -1310,7 +1313,7 @@ k_fgemm1(const S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, f
 template <typename S, int TS, bool CM>
 __global__ void __launch_bounds__(kGT, 1)
 k_fw2x1(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *ws0, int64_t ws_bstride,
-        int64_t n, int nsplit, int nused, int par) {
+        int64_t n, int nsplit, int nused, int par, int w2t) {
     constexpr int BM = TS, BN = 64;
     using TL = Tile<BM, BN>;
     __shared__ __align__(16) float As[2][TL::A_EL];
@@ -1360,18 +1363,24 @@ k_fw2x1(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *w
             const int c = TL::col(tn, h * 4);
             const float4 v = make_float4(acc[ii][h * 4], acc[ii][h * 4 + 1], acc[ii][h * 4 + 2], acc[ii][h * 4 + 3]);
             *reinterpret_cast<float4 *>(&W2s[r * TL::BNP + c]) = v;
-            if (c0 + c < C) *reinterpret_cast<float4 *>(&w.W2[(int64_t)r * C + c0 + c]) = v;
+            if (c0 + c < C) {
+                *reinterpret_cast<float4 *>(&w.W2[(int64_t)r * C + c0 + c]) = v;
+                if (w2t) {   // K-major copy for the tensor-core update: W2T[c][j]
+                    float *t = w.W2T + (int64_t)(c0 + c) * TS + r;
+                    t[0] = v.x; t[TS] = v.y; t[2 * TS] = v.z; t[3 * TS] = v.w;
+                }
+            }
         }
     }
     // pass 2: X[0:TS] -= V[0:TS] W2
     tile_io<S, BM, BN, CM>(X, ld, 0, TS, c0, C, tm, tn, acc, false);
-    la.fetch(Vcm, M, 0, TS, 0, TS);
+    la.fetch(Vcm, n, 0, TS, 0, TS);
     la.commit(As[0], BM);
     __syncthreads();
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
         const int cur = ch & 1;
-        if (ch + 1 < NCH) la.fetch(Vcm, M, (ch + 1) * KC, TS, 0, TS);
+        if (ch + 1 < NCH) la.fetch(Vcm, n, (ch + 1) * KC, TS, 0, TS);
         TL::template mma<true>(As[cur], W2s + ch * KC * TL::BNP, acc, tm, tn);
         if (ch + 1 < NCH) la.commit(As[cur ^ 1], BM);
         __syncthreads();
@@ -1383,7 +1392,7 @@ k_fw2x1(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *w
 // order) and builds T (compact WY, forward) -> w.T row-major.
 template <int TS>
 __global__ void __launch_bounds__(kGT, 1)
-k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps) {
+k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps, int par) {
     constexpr int BM = TS, BN = TS;
     using TL = Tile<BM, BN>;
     __shared__ __align__(16) float As[2][TL::A_EL];
@@ -1394,6 +1403,7 @@ k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps) {
     const Ws w = ws_carve(ws0 + (int64_t)b * ws_bstride, n, TS, nsplit);
     const int sp = blockIdx.x, ns = gridDim.x;
     const int k_lo = sp * rps, k_hi = min(M, k_lo + rps);
+    const float *Vrm = w.vrm(par);
     int tm, tn;
     tmtn<false>(tm, tn);
     float acc[TL::TM][TL::TN];
@@ -1404,8 +1414,8 @@ k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps) {
     LdKM<float, BM> la;
     LdKM<float, BN> lb;
     if (k_lo < k_hi) {
-        la.fetch(w.Vrm, TS, k_lo, k_hi, 0, TS);
-        lb.fetch(w.Vrm, TS, k_lo, k_hi, 0, TS);
+        la.fetch(Vrm, TS, k_lo, k_hi, 0, TS);
+        lb.fetch(Vrm, TS, k_lo, k_hi, 0, TS);
         la.commit(As[0], BM);
         lb.commit(Bs[0], TL::BNP);
         __syncthreads();
@@ -1414,8 +1424,8 @@ k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps) {
         for (int ch = 0; ch < nch; ++ch) {
             const int cur = ch & 1;
             if (ch + 1 < nch) {
-                la.fetch(w.Vrm, TS, k_lo + (ch + 1) * KC, k_hi, 0, TS);
-                lb.fetch(w.Vrm, TS, k_lo + (ch + 1) * KC, k_hi, 0, TS);
+                la.fetch(Vrm, TS, k_lo + (ch + 1) * KC, k_hi, 0, TS);
+                lb.fetch(Vrm, TS, k_lo + (ch + 1) * KC, k_hi, 0, TS);
             }
             TL::template mma<false>(As[cur], Bs[cur], acc, tm, tn);
             if (ch + 1 < nch) {
@@ -1449,6 +1459,92 @@ k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps) {
         w.T[e] = (jj >= i) ? Tsm[jj * LDT + i] : 0.f;
     }
     if (threadIdx.x == 0) *w.cnt = 0;
+}
+
+
+// ---------------------------------------------------------------------------
+// k_tbuild: T (compact WY, forward) of the whole panel from the Gram matrix
+// G = V^T V that the tensor-core W product computed as its extra column tile
+// (ns split-K partials, summed here in a fixed order) and tau:
+//   diagonal 32 x 32 blocks by the row-parallel recurrence (lane i owns row i:
+//     T[i][j] = -tau_j sum_{i<=c<j} T[i][c] G[c][j]),
+//   then two merge levels T12 = -T11 (G12 T22) of 32- and 64-wide blocks.
+// One CTA of 256 threads per batch member; w.T row-major, zero below the
+// diagonal (the layout k_fw2x1 reads).
+constexpr int kTB = 256;
+template <int TS>
+__global__ void __launch_bounds__(kTB, 1) k_tbuild(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int ns) {
+    static_assert(TS == 128, "k_tbuild: ts = 128");
+    constexpr int LD = TS + 1;
+    extern __shared__ float tsm[];
+    float *G = tsm;                 // [TS][LD]
+    float *T = G + TS * LD;         // [TS][LD]
+    float *Xs = T + TS * LD;        // [64][65] product scratch
+    const Ws w = ws_carve(ws0 + (int64_t)blockIdx.x * ws_bstride, n, TS, nsplit);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int e4 = tid * 4; e4 < TS * TS; e4 += kTB * 4) {
+        float4 acc = f4zero();
+        for (int s = 0; s < ns; ++s) {
+            const float4 v = __ldcg(reinterpret_cast<const float4 *>(w.Gp + (int64_t)s * TS * TS + e4));
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        const int i = e4 / TS, j = e4 % TS;
+        G[i * LD + j] = acc.x; G[i * LD + j + 1] = acc.y; G[i * LD + j + 2] = acc.z; G[i * LD + j + 3] = acc.w;
+        T[i * LD + j] = 0.f; T[i * LD + j + 1] = 0.f; T[i * LD + j + 2] = 0.f; T[i * LD + j + 3] = 0.f;
+    }
+    __syncthreads();
+    if (warp < 4) {                 // diagonal block `warp`
+        const int o = warp * 32, i = lane;
+        float tr[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < j; ++c) {
+                const float gcj = G[(o + c) * LD + o + j];
+                if (c & 1) s1 = (c >= i) ? fmaf(tr[c], gcj, s1) : s1;
+                else s0 = (c >= i) ? fmaf(tr[c], gcj, s0) : s0;
+            }
+            const float tj = __ldcg(&w.tau[o + j]);
+            tr[j] = (j < i) ? 0.f : (j == i ? tj : -tj * (s0 + s1));
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) T[(o + i) * LD + o + j] = tr[j];
+    }
+    __syncthreads();
+    // merges: T[a:a+h, b:b+h] = -T[a:a+h, a:a+h] * (G[a:a+h, b:b+h] * T[b:b+h, b:b+h]), b = a + h
+    for (int h = 32; h < TS; h *= 2) {
+        const int nm = TS / (2 * h);               // merges at this level
+        const int per = h * h;                      // outputs per product
+        // X = G12 * T22  (per merge; nm * per <= 4096)
+        for (int e = tid; e < nm * per; e += kTB) {
+            const int mg = e / per, r = (e % per) / h, c = e % h;
+            const int a = mg * 2 * h, bb = a + h;
+            float s0 = 0.f, s1 = 0.f;
+            for (int k = 0; k <= c; k += 2) {       // T22 upper triangular: k <= c
+                s0 = fmaf(G[(a + r) * LD + bb + k], T[(bb + k) * LD + bb + c], s0);
+                if (k + 1 <= c) s1 = fmaf(G[(a + r) * LD + bb + k + 1], T[(bb + k + 1) * LD + bb + c], s1);
+            }
+            Xs[mg * per + r * h + c] = s0 + s1;
+        }
+        __syncthreads();
+        // T12 = -T11 * X  (T11 upper triangular: k >= r)
+        for (int e = tid; e < nm * per; e += kTB) {
+            const int mg = e / per, r = (e % per) / h, c = e % h;
+            const int a = mg * 2 * h, bb = a + h;
+            float s0 = 0.f, s1 = 0.f;
+            for (int k = r; k < h; k += 2) {
+                s0 = fmaf(T[(a + r) * LD + a + k], Xs[mg * per + k * h + c], s0);
+                if (k + 1 < h) s1 = fmaf(T[(a + r) * LD + a + k + 1], Xs[mg * per + (k + 1) * h + c], s1);
+            }
+            T[(a + r) * LD + bb + c] = -(s0 + s1);
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < TS * TS; e += kTB) {
+        const int i = e / TS, j = e % TS;
+        w.T[e] = (j >= i) ? T[i * LD + j] : 0.f;
+    }
 }
 
 __global__ void k_zero_cnt(float *ws0, int64_t ws_bstride, int64_t n, int ts, int nsplit, int64_t batch) {
@@ -1564,6 +1660,21 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         cudaEventRecord(tp0, sp);
     }
     int par = 0;
+    const bool use_tc = TS == 128 && flat_tc_supported(TS, (int)sizeof(S));
+    FlatTcPlan *tcp = nullptr;
+    const size_t tbuild_smem = (2 * (size_t)TS * (TS + 1) + 64 * 65) * sizeof(float);
+    if (use_tc) {
+        if constexpr (TS == 128)
+            if ((e = ensure_smem(k_tbuild<TS>, tbuild_smem)) != cudaSuccess) return e;
+        const Ws w0 = ws_carve(ws, n, TS, nsplit);
+        tcp = flat_tc_plan(reinterpret_cast<float *>(a), n, batch, a_bstride, w0.Vcm0, w0.Vcm1, w0.Vrm0, w0.Vrm1,
+                           w0.W2T, wsb);
+        if (!tcp) return cudaErrorNotSupported;
+    }
+    // development knob: BSVD_FLAT_TC=2 -> only the W product on the tensor
+    // cores, 3 -> only the X update
+    const int tc_sel = getenv("BSVD_FLAT_TC") ? atoi(getenv("BSVD_FLAT_TC")) : 1;
+    const bool tc1 = use_tc && tc_sel != 3, tc2 = use_tc && tc_sel != 2;
     const char *trace_path = getenv("BSVD_FPANEL_TRACE");
     const int trace_side = getenv("BSVD_FPANEL_TRACE_SIDE") ? atoi(getenv("BSVD_FPANEL_TRACE_SIDE")) : 0;
     unsigned long long *trace_buf = nullptr;
@@ -1608,51 +1719,75 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         }
         if (C > 0) {
             cudaEventRecord(evP, sp);
-            // T from V^T V (overlaps the first product on the update stream)
-            const int gs = (int)std::min<int64_t>(kGSplit, std::max<int64_t>(1, M / 512));
-            const int grps = ((M + gs - 1) / gs + KC - 1) / KC * KC;
-            k_fgram<TS><<<dim3((unsigned)gs, (unsigned)batch), kGT, (TS * (TS + 1) + TS * TS / 4) * sizeof(float), sp>>>(
-                ws, wsb, n, nsplit, M, grps);
-            bsvd_host::count_launch();
-            if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            if (!tc1) {   // T from V^T V (overlaps the first product on the update stream)
+                const int gs = (int)std::min<int64_t>(kGSplit, std::max<int64_t>(1, M / 512));
+                const int grps = ((M + gs - 1) / gs + KC - 1) / KC * KC;
+                k_fgram<TS><<<dim3((unsigned)gs, (unsigned)batch), kGT, (TS * (TS + 1) + TS * TS / 4) * sizeof(float), sp>>>(
+                    ws, wsb, n, nsplit, M, grps, par);
+                bsvd_host::count_launch();
+                if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            }
             // W partials over row splits
             const int cblk = (C + 127) / 128;
             int ns = 1;
             if (batch == 1) {
-                ns = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, (2 * 148 + cblk - 1) / cblk));
+                ns = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, ((tc1 ? 1 : 2) * 148 + cblk - 1) / cblk));
                 ns = std::min(ns, std::max(1, M / 256));
+                if (tc1 && getenv("BSVD_TC_NS")) ns = std::max(1, std::min(nsplit, std::min(M / 32, atoi(getenv("BSVD_TC_NS")))));
             }
-            const int rps = ((M + ns - 1) / ns + KC - 1) / KC * KC;
+            const int rps = ((M + ns - 1) / ns + (tc1 ? 31 : KC - 1)) / (tc1 ? 32 : KC) * (tc1 ? 32 : KC);
             cudaStreamWaitEvent(su, evP, 0);
-            if (lq)
+            Ws w0 = ws_carve(ws, n, TS, nsplit);
+            if (tc1)
+            {
+                e2 = launch_flat_tc(tcp, par, 1, lq, M, C, (int)(top * TS), (int)((k + 1) * TS), w0.Wp, w0.Gp, wsb, ns,
+                                    rps, reinterpret_cast<float *>(a), n, a_bstride, batch, su);
+                if (e2 == cudaSuccess) {
+                    if constexpr (TS == 128) {
+                        k_tbuild<TS><<<(unsigned)batch, kTB, tbuild_smem, su>>>(ws, wsb, n, nsplit, ns);
+                        bsvd_host::count_launch();
+                        e2 = cudaGetLastError();
+                    }
+                }
+            }
+            else if (lq)
                 k_fgemm1<S, TS, false><<<dim3((unsigned)cblk, (unsigned)ns, (unsigned)batch), kGT, 0, su>>>(
-                    X, rs, a_bstride, M, C, ws, wsb, n, nsplit, rps);
+                    X, rs, a_bstride, M, C, ws, wsb, n, nsplit, rps, par);
             else
                 k_fgemm1<S, TS, true><<<dim3((unsigned)cblk, (unsigned)ns, (unsigned)batch), kGT, 0, su>>>(
-                    X, cs, a_bstride, M, C, ws, wsb, n, nsplit, rps);
-            bsvd_host::count_launch();
-            if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+                    X, cs, a_bstride, M, C, ws, wsb, n, nsplit, rps, par);
+            if (!tc1) {
+                bsvd_host::count_launch();
+                e2 = cudaGetLastError();
+            }
+            if (e2 != cudaSuccess) return e2;
             cudaEventRecord(ev1, su);
             cudaStreamWaitEvent(sp, ev1, 0);
             const size_t w2sm = TS * (64 + 4) * sizeof(float);
             if (lq)
                 k_fw2x1<S, TS, false><<<dim3((unsigned)((C + 63) / 64), 1, (unsigned)batch), kGT, w2sm, sp>>>(
-                    X, rs, a_bstride, M, C, ws, wsb, n, nsplit, ns, par);
+                    X, rs, a_bstride, M, C, ws, wsb, n, nsplit, ns, par, tc2 ? 1 : 0);
             else
                 k_fw2x1<S, TS, true><<<dim3((unsigned)((C + 63) / 64), 1, (unsigned)batch), kGT, w2sm, sp>>>(
-                    X, cs, a_bstride, M, C, ws, wsb, n, nsplit, ns, par);
+                    X, cs, a_bstride, M, C, ws, wsb, n, nsplit, ns, par, tc2 ? 1 : 0);
             bsvd_host::count_launch();
             if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
             if (M > TS) {
                 cudaEventRecord(evW, sp);
                 cudaStreamWaitEvent(su, evW, 0);
                 const dim3 g2((unsigned)((M - TS + 127) / 128), (unsigned)cblk, (unsigned)batch);
-                if (lq)
+                if (tc2) {
+                    e2 = launch_flat_tc(tcp, par, 2, lq, M, C, (int)(top * TS), (int)((k + 1) * TS), w0.Wp, w0.Gp, wsb,
+                                        1, 0, reinterpret_cast<float *>(a), n, a_bstride, batch, su);
+                    if (e2 != cudaSuccess) return e2;
+                } else if (lq)
                     k_fgemm2<S, TS, false><<<g2, kGT, 0, su>>>(X, rs, a_bstride, M, C, ws, wsb, n, nsplit, par);
                 else
                     k_fgemm2<S, TS, true><<<g2, kGT, 0, su>>>(X, cs, a_bstride, M, C, ws, wsb, n, nsplit, par);
-                bsvd_host::count_launch();
-                if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+                if (!tc2) {
+                    bsvd_host::count_launch();
+                    if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+                }
             }
         }
         par ^= 1;
@@ -1678,6 +1813,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         cudaEventDestroy(tp1);
     }
     if (trace_buf) cudaFree(trace_buf);
+    if (tcp) flat_tc_plan_free(tcp);
     return e;
 }
 
