@@ -16,7 +16,7 @@
 //                         then run the epilogue;
 //   warp 8 (one thread)   issues hi*hi + hi*lo + lo*hi per K = 8 step into the
 //                         TMEM accumulator, returns each stage by tcgen05.commit.
-// Accuracy: measured on this part (scratch/tc_acc_probe.cu) the kind::tf32
+// Accuracy: measured on this part (scripts/tc_acc_probe.cu) the kind::tf32
 // accumulation is unbiased; 3xTF32 products carry ~2^-22 relative error.
 //
 // Orientation: the MMA's M dimension (TMEM lanes) runs along the matrix's
