@@ -14,10 +14,15 @@ GPU") and the values are gathered to all ranks with NCCL inside the step
 (weak scaling).  `--workload batch` runs configs[4] instead: a batch of
 independent 512 x 512 FP32 matrices (ts = 64) sharded across the ranks.
 
+`--gpus N > 1` defaults to the sharded batch (configs[4]) through
+`distributed.svdvals_sharded` (one NCCL all-gather of the values per step).
+
 `--impl reference` times the reference's CPU path -- the bit-exact C port of
 the reference (oracle/, "kind": "port"; the reference is Python+numba with no
-compiled core to link) -- on the host's cores, rank 0 only, on a bounded
-sample of the same workload (one 2048 x 2048 FP32 matrix, ts = 128 per step).
+compiled core to link) -- on the host's cores, rank 0 only.  An 8192^2 run of
+the port takes minutes, so each step times a bounded 2048^2 sample (ts = 128);
+the reported value is the c*n^3 fit of the samples (1024, 2048, 4096)
+extrapolated to the workload's n, marked "extrapolated": true.
 """
 from __future__ import annotations
 
@@ -34,6 +39,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 CPU_SAMPLE_N = 2048
+CPU_FIT_NS = (1024, 2048, 4096)
 
 
 def flop_model(n: int) -> float:
@@ -97,50 +103,114 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline_sample(threads=None):
-    """Time the reference's CPU path (C port, all host threads) on the bounded
-    sample; returns (TFLOP/s, seconds, threads, description)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _port_seconds(n, threads):
+    """One svdvals of an n x n FP32 N(0,1) matrix (ts = 128) on the C port."""
     import numpy as np
     from oracle import oracle as O
     O.lib()
-    th = threads or os.cpu_count() or 1
-    O.set_num_threads(th)
-    a = np.random.default_rng(0xBE7C).standard_normal((CPU_SAMPLE_N, CPU_SAMPLE_N)).astype(np.float32)
+    O.set_num_threads(threads)
+    a = np.random.default_rng(0xBE7C).standard_normal((n, n)).astype(np.float32)
     t0 = time.perf_counter()
     O.svdvals(a, 128)
-    dt = time.perf_counter() - t0
-    desc = (f"reference C port (oracle/bsvd_oracle.c, bit-exact to bandsvd) svdvals of one "
-            f"{CPU_SAMPLE_N}x{CPU_SAMPLE_N} FP32 N(0,1) matrix, ts=128, {th} OpenMP threads; "
-            f"TFLOP/s on the 8/3 n^3 model of the sample")
-    return flop_model(CPU_SAMPLE_N) / dt / 1e12, dt, th, desc
+    return time.perf_counter() - t0
+
+
+def cpu_fit(samples, n_target):
+    """c from t = c n^3 (least squares in log space) -> (seconds at n_target, c)."""
+    import math
+    logc = [math.log(t / float(n) ** 3) for n, t in samples]
+    c = math.exp(sum(logc) / len(logc))
+    return c * float(n_target) ** 3, c
+
+
+def cpu_baseline_fit(n_target, threads=None, extra=()):
+    """The reference's CPU path (C port, all host threads) at 1024/2048/4096,
+    fitted c*n^3 and extrapolated to n_target; returns the cpu_baseline dict."""
+    th = threads or os.cpu_count() or 1
+    pts = [(n, _port_seconds(n, th)) for n in CPU_FIT_NS] + list(extra)
+    t_target, c = cpu_fit(pts, n_target)
+    return {"value": flop_model(n_target) / t_target / 1e12, "unit": "TFLOP/s", "cores": th, "kind": "port",
+            "extrapolated": True, "seconds_at_n": t_target, "n": n_target,
+            "fit": {"model": "t = c n^3", "c": c, "points_s": {str(n): t for n, t in pts}},
+            "cpu_model": cpu_model(),
+            "sample": (f"reference C port (oracle/bsvd_oracle.c, bit-exact to bandsvd) svdvals of "
+                       f"{'/'.join(str(n) for n in CPU_FIT_NS)}^2 FP32 N(0,1) matrices, ts=128, {th} OpenMP "
+                       f"threads, fitted t = c n^3 and extrapolated to n = {n_target}")}
+
+
+def cpu_batch_sample(n, cnt, th):
+    """Seconds for `cnt` independent n^2 FP32 matrices (ts = for_size(n)) on the
+    C port, one after another with all threads each."""
+    import numpy as np
+    from oracle import oracle as O
+    O.lib()
+    O.set_num_threads(th)
+    mats = np.random.default_rng(0xC5).standard_normal((cnt, n, n)).astype(np.float32)
+    ts = O.default_tilesize(n)
+    t0 = time.perf_counter()
+    for i in range(cnt):
+        O.svdvals(mats[i], ts)
+    return time.perf_counter() - t0
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    for _ in range(args.warmup):
-        cpu_baseline_sample()
-    vals, secs = [], []
     th = os.cpu_count() or 1
-    for _ in range(args.steps):
-        v, dt, th, desc = cpu_baseline_sample()
-        vals.append(v)
-        secs.append(dt)
-    v = statistics.median(vals)
+    batch = workload_of(args) == "batch"
+    if batch:
+        # configs[4]: independent 512^2 FP32 matrices (ts = 64); each step runs a
+        # bounded sample of 16 of them on the port (all threads per matrix)
+        n, cnt = args.n or 512, 16
+        one_step = lambda: cpu_batch_sample(n, cnt, th)
+        for _ in range(args.warmup):
+            one_step()
+        step_s = statistics.median([one_step() for _ in range(args.steps)])
+        v = cnt * flop_model(n) / step_s / 1e12
+        base = {"value": v, "unit": "TFLOP/s", "cores": th, "kind": "port", "extrapolated": False,
+                "cpu_model": cpu_model(),
+                "sample": f"reference C port svdvals of {cnt} independent {n}^2 FP32 matrices per step, ts=64, "
+                          f"{th} OpenMP threads per matrix"}
+        cfg = {"workload": f"configs[4] sample: {cnt} of the 4096 independent {n}^2 FP32 matrices per step",
+               "n": n, "tilesize": 64}
+        sample_v = v
+    else:
+        n_target = args.n or 8192
+        for _ in range(args.warmup):
+            _port_seconds(CPU_SAMPLE_N, th)
+        step_s = statistics.median([_port_seconds(CPU_SAMPLE_N, th) for _ in range(args.steps)])
+        base = cpu_baseline_fit(n_target, th, extra=[(CPU_SAMPLE_N, step_s)])
+        v = base["value"]
+        cfg = {"workload": f"configs[1] (n = {n_target}, FP32, ts = 128) extrapolated from bounded CPU "
+                           f"samples: each step one {CPU_SAMPLE_N}^2 svdvals, plus one 1024^2 and one "
+                           "4096^2 for the c*n^3 fit",
+               "n": n_target, "tilesize": 128}
+        sample_v = flop_model(CPU_SAMPLE_N) / step_s / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(secs) * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (N(0,1), seeded)",
-        "config": {"workload": f"bounded CPU sample of configs[1]: {CPU_SAMPLE_N}x{CPU_SAMPLE_N} FP32 "
-                               "(the GPU arm runs 8192x8192 FP32, ts=128)",
-                   "n": CPU_SAMPLE_N, "tilesize": 128},
-        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": th, "kind": "port", "sample": desc},
+        "data": "synthetic (N(0,1), seeded)", "config": cfg, "sample_value": sample_v,
+        "cpu_baseline": dict(base, value=v),
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_of(args):
+    return args.workload or ("batch" if args.gpus > 1 or int(os.environ.get("WORLD_SIZE", 1)) > 1 else "single")
 
 
 def run_b200(args):
@@ -160,33 +230,45 @@ def run_b200(args):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
 
-    if args.workload == "single":
+    from paper_2508_06339_b200 import distributed as D
+    wl = workload_of(args)
+    if wl == "single":
         n = args.n or 8192
         cfg = P.KernelConfig.for_size(n) if not args.ts else P.KernelConfig(tilesize=args.ts)
         x = torch.randn((n, n), generator=gen, device=dev, dtype=torch.float32).to(dtype)
-        units = 1
+        units, total_units = 1, world
         call = lambda inp, timers=None: P.svdvals(inp, cfg, be, timers)
         workload = (f"configs[1]: one {n}x{n} {args.dtype.upper()} N(0,1) matrix per GPU, svdvals "
                     f"(all singular values), default tiles ts={cfg.tilesize}")
+        parallelism = (f"replicas x{world} (a single matrix stays on one GPU; values all-gathered over NCCL)"
+                       if world > 1 else "1 GPU")
+
+        def step(inp, timers=None):
+            vals = call(inp, timers)
+            if world > 1:
+                vt = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(vals).to(dev)
+                out = [torch.empty_like(vt) for _ in range(world)]
+                dist.all_gather(out, vt.contiguous())
+                return out
+            return vals
     else:
         n = args.n or 512
-        total = args.batch or 4096
-        per = total // world
+        total_units = args.batch or 4096
+        lo, hi = D.shard_range(total_units, world, rank)
+        units = hi - lo
         cfg = P.KernelConfig.for_size(n) if not args.ts else P.KernelConfig(tilesize=args.ts)
-        x = torch.randn((per, n, n), generator=gen, device=dev, dtype=torch.float32).to(dtype)
-        units = per
+        # each rank generates its own shard (inputs never cross NVLink)
+        x = torch.randn((units, n, n), generator=gen, device=dev, dtype=torch.float32).to(dtype)
         call = lambda inp, timers=None: P.svdvals_batched(inp, cfg, be, timers)
-        workload = (f"configs[4]: batch of {total} independent {n}x{n} {args.dtype.upper()} matrices "
-                    f"sharded {per} per GPU, ts={cfg.tilesize}")
+        workload = (f"configs[4]: batch of {total_units} independent {n}x{n} {args.dtype.upper()} matrices "
+                    f"sharded {units} per GPU, ts={cfg.tilesize}")
+        parallelism = (f"batch sharded over {world} GPUs (distributed.svdvals_sharded: one NCCL all-gather "
+                       "of the values per step)" if world > 1 else "1 GPU")
 
-    def step(inp, timers=None):
-        vals = call(inp, timers)
-        if world > 1:
-            vt = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(vals).to(dev)
-            out = [torch.empty_like(vt) for _ in range(world)]
-            dist.all_gather(out, vt.contiguous())
-            return out
-        return vals
+        def step(inp, timers=None):
+            if world > 1 and timers is None:
+                return D.svdvals_sharded(cfg=cfg, backend=be, batch=total_units, make_shard=lambda a, b: inp)
+            return call(inp, timers)
 
     for _ in range(max(args.warmup, 1)):
         step(x)
@@ -216,7 +298,7 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    flops_step = flop_model(n) * units * world
+    flops_step = flop_model(n) * total_units
     value = flops_step / (ms * 1e-3) / 1e12
 
     # ---- end to end through the public API with host buffers -------------
@@ -245,67 +327,79 @@ def run_b200(args):
                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                "d2h_bytes_per_step": int(units * n * out_elem)}
 
-    # ---- roofline of the dominant phase (device events over the timed steps)
+    # ---- rooflines (phase spans from device events; per-kernel DRAM traffic
+    # from the committed ncu capture of the same workload, profiles/traffic.json)
     hbm_gbs, smax, peak_src = measured_peaks()
     fp32_peak = 148 * 128 * 2 * smax * 1e6 / 1e12
     fp64_peak = fp32_peak / 2
     per = {k: v / args.steps * 1e3 for k, v in timers.items()}   # ms per step
-    # panel and trailing overlap on two streams: stage 1's wall time is the step
-    # minus the (serial) stage-2/3 spans
+    # panel chain and tensor-core updates overlap on two streams: stage 1's
+    # wall time is the step minus the (serial) stage-2/3 spans
     stage1_ms = max(ms - per["bidiagonal"] - per["diagonal"], 1e-6)
-    walls = {"stage1": stage1_ms, "bidiagonal": per["bidiagonal"], "diagonal": per["diagonal"]}
-    dom = max(walls, key=walls.get)
     bw = cfg.tilesize
     npad = -(-n // bw) * bw
     fpk = fp64_peak if dtype == torch.float64 else fp32_peak
     fpk_src = (f"derived {'FP64' if dtype == torch.float64 else 'FP32'} FMA peak 148 SMs x "
                f"{64 if dtype == torch.float64 else 128} lanes x 2 x {smax:.0f} MHz "
                "(MEASURED_PEAKS.json has no CUDA-core FMA entry)")
+    traffic = {}
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        pass
+    tc_on = dtype == torch.float32 and bw == 128 and os.environ.get("BSVD_FLAT_TC", "1") != "0"
     ach1 = flop_model(n) * units / (stage1_ms * 1e-3) / 1e12
+    s1_model_bytes = 4.0 * npad ** 3 / (3.0 * bw) * (8 if dtype == torch.float64 else
+                                                      2 if dtype == torch.float16 else 4) * units
+    s1_traffic = traffic.get(f"stage1_step_n{n}") if wl == "single" else None
     phases = {
-        "stage1": {"bound": "fma", "kernel": "stage 1 (k_panel_leaf2/k_panel_tt + k_leaf2_u/k_node_tu + k_apply_leaf2/k_apply_tt on 3 streams)",
-                   "achieved": ach1, "peak": fpk, "unit": "TFLOP/s", "frac": ach1 / fpk,
-                   "peak_source": fpk_src, "model": "8/3 n^3 flops (the reference's count)", "traffic": None},
+        "stage1": {"bound": "fma", "achieved": ach1, "peak": fpk, "unit": "TFLOP/s", "frac": ach1 / fpk,
+                   "kernel": ("stage 1: k_fpanel2 (cluster Householder panel) + k_tgemm (tcgen05 3xTF32 W = V^T X "
+                              "and X -= V W2, TMA-fed) + k_tbuild + k_fw2x1" if tc_on else
+                              "stage 1: k_fpanel2 + k_fgemm1/k_fgemm2 (FMA) + k_fgram + k_fw2x1"),
+                   "peak_source": fpk_src, "model": "8/3 n^3 flops (the reference's count) over the stage-1 span",
+                   "algorithmic_bytes": s1_model_bytes,
+                   "bytes_model": "4 n^3/(3 ts) x elem: the trailing matrix read + written once per sweep side",
+                   "traffic": s1_traffic},
     }
     # stage 2 chases in the compute precision (fp32 band for FP32/FP16, fp64 for FP64)
     belem = 8 if dtype == torch.float64 else 4
     algo_bytes = 2.0 * bw * npad * npad * belem * units
     ach2 = algo_bytes / (per["bidiagonal"] * 1e-3) / 1e9
     if bw > 64:
-        chase_k = "k_chase2 (stage 2, carried-block cluster chase, one launch)"
+        chase_k = "k_chase2"
+        chase_d = "k_chase2 (stage 2, carried-block cluster chase, one launch)"
     elif units >= 512:
-        chase_k = "k_chase_cta (stage 2, one CTA per matrix, carried blocks in registers)"
+        chase_k, chase_d = "k_chase_cta", "k_chase_cta (stage 2, one CTA per matrix, carried blocks in registers)"
     else:
-        chase_k = "k_chase (stage 2, pipelined cluster chase)"
-    phases["bidiagonal"] = {"bound": "hbm", "kernel": chase_k,
+        chase_k, chase_d = "k_chase", "k_chase (stage 2, pipelined cluster chase)"
+    phases["bidiagonal"] = {"bound": "hbm", "kernel": chase_d,
                             "achieved": ach2, "peak": hbm_gbs, "unit": "GB/s", "frac": ach2 / hbm_gbs,
                             "peak_source": peak_src, "algorithmic_bytes": algo_bytes,
-                            "model": f"touch model 2*bw*n^2*{belem} B per matrix (SURVEY.md 8(d))", "traffic": None}
-    # stage 3: counted Sturm steps are not fixed; report time against the FP64 pipe
-    # on a 64-count-per-value model of plain bisection (the work it replaces)
-    algo3 = units * n * 64 * 2 * npad * 10.0
-    ach3 = algo3 / (per["diagonal"] * 1e-3) / 1e12
-    phases["diagonal"] = {"bound": "fma", "kernel": "k_slice + k_values (stage 3)", "achieved": ach3,
-                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach3 / fp64_peak,
-                          "peak_source": "derived FP64 FMA peak",
-                          "model": "64 Sturm counts x 2n steps x 10 flops per value (bisection-equivalent)",
-                          "traffic": None}
-    roof = dict(phases[dom])
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            tr = json.load(open(prof))
-            roof["traffic"] = tr.get(roof["kernel"].split()[0])
-            for ph in phases.values():
-                ph["traffic"] = tr.get(ph["kernel"].split()[0])
-        except Exception:
-            pass
+                            "model": f"touch model 2*bw*n^2*{belem} B per matrix (SURVEY.md 8(d)); the band "
+                                     "(3b+1 rows) stays L2-resident, so the kernel is bound by its sweep "
+                                     "dependency chain, not by DRAM",
+                            "traffic": traffic.get(chase_k) if wl == "single" else None}
+    # stage 3: the number of Sturm passes per value is data dependent; no flop
+    # model -- time only
+    phases["diagonal"] = {"bound": "latency", "kernel": "k_slice + k_values (stage 3, fp64 Sturm counts)",
+                          "ms": per["diagonal"], "achieved": None, "peak": None, "frac": None,
+                          "traffic": traffic.get("k_values") if wl == "single" else None}
+    # the required roofline object: the largest single kernel of the step (the
+    # chase is one launch, timed live by its device events)
+    roof = dict(phases["bidiagonal"])
+    roof["kernel"] = chase_d
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, dt, th, desc = cpu_baseline_sample()
-        cpu = {"value": v, "unit": "TFLOP/s", "cores": th, "kind": "port", "sample": desc,
-               "seconds": dt}
+        if wl == "single":
+            cpu = cpu_baseline_fit(n)
+        else:
+            th = os.cpu_count() or 1
+            dt = cpu_batch_sample(n, 16, th)
+            cpu = {"value": 16 * flop_model(n) / dt / 1e12, "unit": "TFLOP/s", "cores": th, "kind": "port",
+                   "extrapolated": False, "cpu_model": cpu_model(), "seconds": dt,
+                   "sample": f"reference C port svdvals of 16 independent {n}^2 FP32 matrices, {th} OpenMP threads"}
 
     if rank == 0:
         line = {
@@ -315,10 +409,10 @@ def run_b200(args):
             "dtype": {"fp32": "f32", "fp64": "f64", "fp16": "f16-storage/f32-compute"}[args.dtype],
             "data": "synthetic (N(0,1) random, seeded per rank; no dataset)",
             "config": {"workload": workload, "n": n, "tilesize": cfg.tilesize, "units_per_gpu": units,
-                       "parallelism": f"replicas x{world} (values all-gathered over NCCL)" if world > 1 else "1 GPU",
+                       "parallelism": parallelism,
                        "l2": "inputs larger than L2 (the padded working copy is rewritten every step)"},
             "stages_ms": per, "stage1_wall_ms": stage1_ms,
-            "stage1_tflops": flop_model(n) * units / (stage1_ms * 1e-3) / 1e12,
+            "stage1_tflops": ach1,
             "roofline": roof, "phase_roofline": phases, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
@@ -336,7 +430,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["single", "batch"], default="single")
+    ap.add_argument("--workload", choices=["single", "batch"], default=None,
+                    help="default: single on 1 GPU, the sharded batch (configs[4]) on N > 1")
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--ts", type=int, default=0)
     ap.add_argument("--batch", type=int, default=0)
