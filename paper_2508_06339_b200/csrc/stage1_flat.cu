@@ -522,8 +522,8 @@ k_fpanel(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, fl
 namespace p2 {
 // development instrumentation (BSVD_FPANEL_TRACE): phase timestamps of CTA 0
 __device__ unsigned long long *g_trace = nullptr;
-__device__ __forceinline__ void stamp(int i) {
-    if (g_trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+__device__ __forceinline__ void stamp(int i, int who = 0) {
+    if (g_trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == who) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_trace[i] = t;
@@ -620,8 +620,9 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
     __shared__ __align__(16) float slot[2][kMaxCS][32];
     __shared__ __align__(16) float pslot[2][32];
     __shared__ __align__(16) float prow[2][32];
-    __shared__ float Y[NB][NB + 1];
     __shared__ __align__(16) float Ts[NB][NB + 1];
+    __shared__ float Y[NB][NB + 1];
+    __shared__ float Xm[2 * 8 * 8 + 16 * 16];
     __shared__ float taus[NB];
     __shared__ __align__(8) uint64_t mbar[4];   // [0,1] column exchange, [2] RS, [3] AG
     extern __shared__ __align__(16) float dsm[];
@@ -776,7 +777,7 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
                 const float wv = fmaf(g, scale, pr);   // v_j^T x_l (l > j) / v_l^T v_j (l < j)
                 const float fco = lane > j ? tau * wv : 0.f;
                 if (warp == 0) {
-                    if (lane < j) Y[j][lane] = wv;
+                    if (lane < j) Y[j][lane] = wv;   // v_l^T v_j, l < j
                     if (lane == 0) taus[j] = tau;
                 }
                 float f[8];
@@ -792,28 +793,48 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
                 }
             }
         }
-        __syncthreads();   // Y, taus complete
+        __syncthreads();   // T_s, taus complete
         p2::stamp(1 + s * 12 + 4);
 
-        // ---- write back R / tails, clean V -> Vrm, Vcm; T_s by warp 0 -------
-        if (warp == 0) {
-            float tr[NB];
-            const int i = lane;
+        // ---- T_s (compact WY of the sub-panel) by block recursion: 8 x 8
+        // diagonal blocks (one warp each), then T12 = -T11 (G12 T22) merges
+        // with G[c][j] = v_c^T v_j = Y[j][c]; ~1k cycles on the whole CTA -----
+        if (warp < 4 && lane < 8) {
+            const int o = warp * 8, i = lane;
+            float tr[8];
 #pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                float s0 = 0.f, s1 = 0.f;
+            for (int j = 0; j < 8; ++j) {
+                float acc = 0.f;
 #pragma unroll
-                for (int c = 0; c < j; ++c) {
-                    const float y = Y[j][c];
-                    if (c & 1) s1 = (c >= i) ? fmaf(tr[c], y, s1) : s1;
-                    else s0 = (c >= i) ? fmaf(tr[c], y, s0) : s0;
-                }
-                tr[j] = (j < i) ? 0.f : (j == i ? taus[j] : -taus[j] * (s0 + s1));
+                for (int c = 0; c < j; ++c) acc = (c >= i) ? fmaf(tr[c], Y[o + j][o + c], acc) : acc;
+                tr[j] = (j < i) ? 0.f : (j == i ? taus[o + j] : -taus[o + j] * acc);
             }
 #pragma unroll
-            for (int j = 0; j < NB; ++j) Ts[i][j] = tr[j];
-            if (rank == 0) w.tau[col0 + lane] = taus[lane];
+            for (int j = 0; j < 8; ++j) Ts[o + i][o + j] = tr[j];
         }
+        if (warp == 0 && rank == 0) w.tau[col0 + lane] = taus[lane];
+        __syncthreads();
+#pragma unroll
+        for (int h = 8; h < NB; h *= 2) {
+            const int nm = NB / (2 * h), per = h * h;
+            if (tid < nm * per) {      // X = G12 T22 (T22 upper triangular)
+                const int mg = tid / per, r = (tid % per) / h, c = tid % h;
+                const int a = mg * 2 * h, bb = a + h;
+                float acc = 0.f;
+                for (int k = 0; k <= c; ++k) acc = fmaf(Y[bb + k][a + r], Ts[bb + k][bb + c], acc);
+                Xm[tid] = acc;
+            }
+            __syncthreads();
+            if (tid < nm * per) {      // T12 = -T11 X (T11 upper triangular)
+                const int mg = tid / per, r = (tid % per) / h, c = tid % h;
+                const int a = mg * 2 * h, bb = a + h;
+                float acc = 0.f;
+                for (int k = r; k < h; ++k) acc = fmaf(Ts[a + r][a + k], Xm[mg * per + k * h + c], acc);
+                Ts[a + r][bb + c] = -acc;
+            }
+            __syncthreads();
+        }
+        // ---- write back R, clean V -> Vrm, Vcm -----------------------------
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
             const int r = rbase + 128 * i;
@@ -845,6 +866,7 @@ k_fpanel2(S *__restrict__ P, int64_t rs, int64_t cs, int64_t a_bstride, int M, f
 #pragma unroll
             for (int c = 0; c < 8; ++c) a[i][c] = v[c];   // a := clean V from here on
         }
+        p2::stamp(1 + s * 12 + 10, 32);   // warp 1's write-back done
         p2::stamp(1 + s * 12 + 5);
         if (s == TS / NB - 1) break;
 
@@ -1484,9 +1506,13 @@ __global__ void __launch_bounds__(kTB, 1) k_tbuild(float *ws0, int64_t ws_bstrid
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int e4 = tid * 4; e4 < TS * TS; e4 += kTB * 4) {
         float4 acc = f4zero();
-        for (int s = 0; s < ns; ++s) {
-            const float4 v = __ldcg(reinterpret_cast<const float4 *>(w.Gp + (int64_t)s * TS * TS + e4));
-            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        float4 v[kGSplit];
+#pragma unroll
+        for (int s = 0; s < kGSplit; ++s)
+            v[s] = s < ns ? __ldcg(reinterpret_cast<const float4 *>(w.Gp + (int64_t)s * TS * TS + e4)) : f4zero();
+#pragma unroll
+        for (int s = 0; s < kGSplit; ++s) {   // fixed order
+            acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
         }
         const int i = e4 / TS, j = e4 % TS;
         G[i * LD + j] = acc.x; G[i * LD + j + 1] = acc.y; G[i * LD + j + 2] = acc.z; G[i * LD + j + 3] = acc.w;
@@ -1512,34 +1538,61 @@ __global__ void __launch_bounds__(kTB, 1) k_tbuild(float *ws0, int64_t ws_bstrid
         for (int j = 0; j < 32; ++j) T[(o + i) * LD + o + j] = tr[j];
     }
     __syncthreads();
-    // merges: T[a:a+h, b:b+h] = -T[a:a+h, a:a+h] * (G[a:a+h, b:b+h] * T[b:b+h, b:b+h]), b = a + h
+    // merges: T[a:a+h, b:b+h] = -T[a:a+h, a:a+h] * (G[a:a+h, b:b+h] * T[b:b+h, b:b+h]), b = a + h;
+    // 4 x 4 register tiles per thread (independent accumulators, the K loop
+    // streams one A column and one B row per step)
     for (int h = 32; h < TS; h *= 2) {
         const int nm = TS / (2 * h);               // merges at this level
-        const int per = h * h;                      // outputs per product
-        // X = G12 * T22  (per merge; nm * per <= 4096)
-        for (int e = tid; e < nm * per; e += kTB) {
-            const int mg = e / per, r = (e % per) / h, c = e % h;
-            const int a = mg * 2 * h, bb = a + h;
-            float s0 = 0.f, s1 = 0.f;
-            for (int k = 0; k <= c; k += 2) {       // T22 upper triangular: k <= c
-                s0 = fmaf(G[(a + r) * LD + bb + k], T[(bb + k) * LD + bb + c], s0);
-                if (k + 1 <= c) s1 = fmaf(G[(a + r) * LD + bb + k + 1], T[(bb + k + 1) * LD + bb + c], s1);
+        const int tpr = h / 4;                      // tiles per row
+        const int ntile = nm * tpr * tpr;           // <= 256
+        const int LX = h + 1;
+        for (int pass = 0; pass < 2; ++pass) {
+            if (tid < ntile) {
+                const int mg = tid / (tpr * tpr), rem = tid % (tpr * tpr);
+                const int r0 = (rem / tpr) * 4, c0 = (rem % tpr) * 4;
+                const int a = mg * 2 * h, bb = a + h;
+                float acc[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+                float *X = Xs + mg * h * LX;
+                if (pass == 0) {   // X = G12 * T22 (T22 upper triangular: rows k <= c0 + 3)
+                    for (int k = 0; k <= c0 + 3; ++k) {
+                        float av[4], bv[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) av[i] = G[(a + r0 + i) * LD + bb + k];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) bv[j] = T[(bb + k) * LD + bb + c0 + j];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) X[(r0 + i) * LX + c0 + j] = acc[i][j];
+                } else {           // T12 = -T11 * X (T11 upper triangular: columns k >= r0)
+                    for (int k = r0; k < h; ++k) {
+                        float av[4], bv[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) av[i] = T[(a + r0 + i) * LD + a + k];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) bv[j] = X[k * LX + c0 + j];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) T[(a + r0 + i) * LD + bb + c0 + j] = -acc[i][j];
+                }
             }
-            Xs[mg * per + r * h + c] = s0 + s1;
+            __syncthreads();
         }
-        __syncthreads();
-        // T12 = -T11 * X  (T11 upper triangular: k >= r)
-        for (int e = tid; e < nm * per; e += kTB) {
-            const int mg = e / per, r = (e % per) / h, c = e % h;
-            const int a = mg * 2 * h, bb = a + h;
-            float s0 = 0.f, s1 = 0.f;
-            for (int k = r; k < h; k += 2) {
-                s0 = fmaf(T[(a + r) * LD + a + k], Xs[mg * per + k * h + c], s0);
-                if (k + 1 < h) s1 = fmaf(T[(a + r) * LD + a + k + 1], Xs[mg * per + (k + 1) * h + c], s1);
-            }
-            T[(a + r) * LD + bb + c] = -(s0 + s1);
-        }
-        __syncthreads();
     }
     for (int e = tid; e < TS * TS; e += kTB) {
         const int i = e / TS, j = e % TS;
@@ -1662,7 +1715,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
     int par = 0;
     const bool use_tc = TS == 128 && flat_tc_supported(TS, (int)sizeof(S));
     FlatTcPlan *tcp = nullptr;
-    const size_t tbuild_smem = (2 * (size_t)TS * (TS + 1) + 64 * 65) * sizeof(float);
+    const size_t tbuild_smem = (2 * (size_t)TS * (TS + 1) + 64 * 65 + 64) * sizeof(float);
     if (use_tc) {
         if constexpr (TS == 128)
             if ((e = ensure_smem(k_tbuild<TS>, tbuild_smem)) != cudaSuccess) return e;
