@@ -150,6 +150,16 @@ bsvd_status bsvd_geqrt(void *tile, int64_t rs, int64_t cs, bsvd_dtype dtype, int
 bsvd_status bsvd_tsqrt_chain(void *r, int64_t rs, int64_t cs, void *const *b_tiles,
                              void *const *taus, int32_t nb, bsvd_dtype dtype, int32_t ts,
                              void *stream);
+/* kernels.py:459-470 geqrt_splitk (geqrt_splitk_kernel :233-283): the tile
+ * QR with each column's norm and dot products split over `splitk` row
+ * segments and combined by _pairwise_sum (:191-199); splitk in
+ * [1, min(ts, 1024/ts)], bitwise equal to bsvd_geqrt at splitk == 1. */
+bsvd_status bsvd_geqrt_splitk(void *tile, int64_t rs, int64_t cs, bsvd_dtype dtype, int32_t ts, int32_t splitk,
+                              void *tau, void *stream);
+/* kernels.py:479-481 tsqrt_splitk / :503-515 _tsqrt_chain_splitk
+ * (tsqrt_splitk_kernel :316-361), same segment / pairwise sums. */
+bsvd_status bsvd_tsqrt_chain_splitk(void *r, int64_t rs, int64_t cs, void *const *b_tiles, void *const *taus,
+                                    int32_t nb, bsvd_dtype dtype, int32_t ts, int32_t splitk, void *stream);
 /* kernels.py:518-532 unmqr */
 bsvd_status bsvd_unmqr(const void *panel, int64_t rs, int64_t cs, const void *tau, void *x,
                        int64_t xrs, int64_t xcs, int64_t ncols, bsvd_dtype dtype, int32_t ts,

@@ -419,7 +419,7 @@ void oracle_dense_bidiagonalize(double *A, int64_t n, double *d, double *e) {
  * Returns 0 or -1 (ConvergenceError). */
 #define PIPE(SUF_, S_, C_, LDX, STX)                                                  \
     static int pipeline##SUF_(const S_ *a, int64_t n, int ts, double *vals,            \
-                              S_ *band_out, double *d_out, double *e_out) {            \
+                              S_ *band_out, double *d_out, double *e_out, int nsplit) {\
         int N = (int)((n + ts - 1) / ts);                                               \
         if (N < 1) N = 1;                                                              \
         int64_t np_ = (int64_t)N * ts;                                                  \
@@ -427,7 +427,7 @@ void oracle_dense_bidiagonalize(double *A, int64_t n, double *d, double *e) {
         for (int64_t c = 0; c < n; ++c)                                                 \
             memcpy(w + c * np_, a + c * n, sizeof(S_) * (size_t)n);                     \
         C_ *tau = (C_ *)calloc((size_t)ts * 2 * N * N, sizeof(C_));                     \
-        oracle_banddiag##SUF_(w, N, ts, tau);                                           \
+        oracle_banddiag##SUF_(w, N, ts, tau, nsplit);                                   \
         if (band_out) memcpy(band_out, w, sizeof(S_) * (size_t)(np_ * np_));            \
         double *d = (double *)malloc(sizeof(double) * np_);                             \
         double *e = (double *)calloc((size_t)(np_ > 1 ? np_ - 1 : 1), sizeof(double));  \
@@ -465,31 +465,39 @@ PIPE(_f64, double, double, IDENT, IDENT)
 PIPE(_f32, float, float, IDENT, IDENT)
 PIPE(_f16, uint16_t, float, h2f, f2h)
 
-int oracle_svdvals(int prec, const void *a, int64_t n, int ts, double *vals,
-                   void *band_out, double *d_out, double *e_out) {
+int oracle_svdvals_splitk(int prec, const void *a, int64_t n, int ts, double *vals,
+                          void *band_out, double *d_out, double *e_out, int splitk) {
     switch (prec) {
-    case 1: return pipeline_f64((const double *)a, n, ts, vals, (double *)band_out, d_out, e_out);
-    case 2: return pipeline_f32((const float *)a, n, ts, vals, (float *)band_out, d_out, e_out);
-    case 3: return pipeline_f16((const uint16_t *)a, n, ts, vals, (uint16_t *)band_out, d_out, e_out);
+    case 1: return pipeline_f64((const double *)a, n, ts, vals, (double *)band_out, d_out, e_out, splitk);
+    case 2: return pipeline_f32((const float *)a, n, ts, vals, (float *)band_out, d_out, e_out, splitk);
+    case 3: return pipeline_f16((const uint16_t *)a, n, ts, vals, (uint16_t *)band_out, d_out, e_out, splitk);
     default: return -2;
     }
 }
+int oracle_svdvals(int prec, const void *a, int64_t n, int ts, double *vals,
+                   void *band_out, double *d_out, double *e_out) {
+    return oracle_svdvals_splitk(prec, a, n, ts, vals, band_out, d_out, e_out, 1);
+}
 
 /* Stage-1 only (for timing samples and band parity): a is the padded
- * column-major N*ts square, overwritten with the band; tau zeroed store. */
-void oracle_banddiag(int prec, void *a, int N, int ts, void *tau) {
+ * column-major N*ts square, overwritten with the band; tau zeroed store.
+ * splitk > 1: the split-K panel kernels (kernels.py:233-361). */
+void oracle_banddiag_splitk(int prec, void *a, int N, int ts, void *tau, int splitk) {
     switch (prec) {
-    case 1: oracle_banddiag_f64((double *)a, N, ts, (double *)tau); break;
-    case 2: oracle_banddiag_f32((float *)a, N, ts, (float *)tau); break;
-    case 3: oracle_banddiag_f16((uint16_t *)a, N, ts, (float *)tau); break;
+    case 1: oracle_banddiag_f64((double *)a, N, ts, (double *)tau, splitk); break;
+    case 2: oracle_banddiag_f32((float *)a, N, ts, (float *)tau, splitk); break;
+    case 3: oracle_banddiag_f16((uint16_t *)a, N, ts, (float *)tau, splitk); break;
     }
 }
+void oracle_banddiag(int prec, void *a, int N, int ts, void *tau) { oracle_banddiag_splitk(prec, a, N, ts, tau, 1); }
 
-/* Kernel-level entry points (column-major ts x ts tiles, compute-dtype tau). */
-void oracle_geqrt(int prec, void *a, int ts, void *tau) {
+/* Kernel-level entry points (column-major ts x ts tiles, compute-dtype tau);
+ * splitk > 1: geqrt_splitk (kernels.py:459-470). */
+void oracle_geqrt_splitk(int prec, void *a, int ts, void *tau, int splitk) {
     switch (prec) {
-    case 1: oracle_geqrt_f64((double *)a, 1, ts, ts, (double *)tau); break;
-    case 2: oracle_geqrt_f32((float *)a, 1, ts, ts, (float *)tau); break;
-    case 3: oracle_geqrt_f16((uint16_t *)a, 1, ts, ts, (float *)tau); break;
+    case 1: oracle_geqrt_f64((double *)a, 1, ts, ts, (double *)tau, splitk); break;
+    case 2: oracle_geqrt_f32((float *)a, 1, ts, ts, (float *)tau, splitk); break;
+    case 3: oracle_geqrt_f16((uint16_t *)a, 1, ts, ts, (float *)tau, splitk); break;
     }
 }
+void oracle_geqrt(int prec, void *a, int ts, void *tau) { oracle_geqrt_splitk(prec, a, ts, tau, 1); }

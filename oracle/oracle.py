@@ -50,6 +50,12 @@ def lib():
         L.oracle_banddiag.restype = None
         L.oracle_geqrt.argtypes = [i32, vp, i32, vp]
         L.oracle_geqrt.restype = None
+        L.oracle_geqrt_splitk.argtypes = [i32, vp, i32, vp, i32]
+        L.oracle_geqrt_splitk.restype = None
+        L.oracle_svdvals_splitk.argtypes = [i32, vp, i64, i32, dp, vp, dp, dp, i32]
+        L.oracle_svdvals_splitk.restype = i32
+        L.oracle_banddiag_splitk.argtypes = [i32, vp, i32, i32, vp, i32]
+        L.oracle_banddiag_splitk.restype = None
         L.oracle_bidiagonal_values.argtypes = [dp, dp, i64]
         L.oracle_bidiagonal_values.restype = i32
         L.oracle_num_threads.restype = i32
@@ -78,7 +84,7 @@ def default_tilesize(n: int) -> int:
     return ts
 
 
-def svdvals(a, ts: int | None = None, return_stages: bool = False):
+def svdvals(a, ts: int | None = None, return_stages: bool = False, splitk: int = 1):
     """All singular values, descending, in the compute dtype (FP16 -> float32).
 
     ``a`` is a square array whose dtype selects the precision (float64 /
@@ -103,10 +109,10 @@ def svdvals(a, ts: int | None = None, return_stages: bool = False):
     band = np.zeros(npad * npad, a.dtype) if return_stages else None
     d = np.zeros(npad, np.float64) if return_stages else None
     e = np.zeros(max(npad - 1, 1), np.float64) if return_stages else None
-    rc = lib().oracle_svdvals(PREC_OF_DTYPE[a.dtype], _ptr(src), n, ts, _ptr(vals),
-                              _ptr(band) if band is not None else None,
-                              _ptr(d) if d is not None else None,
-                              _ptr(e) if e is not None else None)
+    rc = lib().oracle_svdvals_splitk(PREC_OF_DTYPE[a.dtype], _ptr(src), n, ts, _ptr(vals),
+                                     _ptr(band) if band is not None else None,
+                                     _ptr(d) if d is not None else None,
+                                     _ptr(e) if e is not None else None, int(splitk))
     if rc != 0:
         raise ArithmeticError("bidiagonal value iteration exceeded its sweep budget")
     out = vals.astype(COMPUTE_OF_STORAGE[a.dtype])
@@ -115,22 +121,24 @@ def svdvals(a, ts: int | None = None, return_stages: bool = False):
     return out
 
 
-def banddiag(a_padded_colmajor: np.ndarray, ts: int):
-    """Stage 1 in place on a padded Fortran-order square; returns the tau store."""
+def banddiag(a_padded_colmajor: np.ndarray, ts: int, splitk: int = 1):
+    """Stage 1 in place on a padded Fortran-order square; returns the tau store
+    (splitk > 1: the split-K panel kernels, kernels.py:233-361)."""
     a = a_padded_colmajor
     assert a.flags.f_contiguous and a.shape[0] == a.shape[1] and a.shape[0] % ts == 0
     N = a.shape[0] // ts
     tau = np.zeros(ts * 2 * N * N, COMPUTE_OF_STORAGE[a.dtype])
-    lib().oracle_banddiag(PREC_OF_DTYPE[a.dtype], _ptr(a), N, ts, _ptr(tau))
+    lib().oracle_banddiag_splitk(PREC_OF_DTYPE[a.dtype], _ptr(a), N, ts, _ptr(tau), int(splitk))
     return tau.reshape((ts, 2 * N * N), order="F")
 
 
-def geqrt(tile: np.ndarray):
-    """Tile QR in place (Fortran-order ts x ts); returns tau (compute dtype)."""
+def geqrt(tile: np.ndarray, splitk: int = 1):
+    """Tile QR in place (Fortran-order ts x ts); returns tau (compute dtype).
+    splitk > 1: geqrt_splitk (kernels.py:459-470)."""
     assert tile.flags.f_contiguous
     ts = tile.shape[0]
     tau = np.zeros(ts, COMPUTE_OF_STORAGE[tile.dtype])
-    lib().oracle_geqrt(PREC_OF_DTYPE[tile.dtype], _ptr(tile), ts, _ptr(tau))
+    lib().oracle_geqrt_splitk(PREC_OF_DTYPE[tile.dtype], _ptr(tile), ts, _ptr(tau), int(splitk))
     return tau
 
 

@@ -37,6 +37,44 @@ static inline void FN(reflector_scalars)(C piv, C sigma, C aik, C rho, C eps10, 
     *x_out = x; *tau_out = tau; *rhop_out = rhop;
 }
 
+/* Split-K sum of x[j]*y[j] over rows [lo, ts) (kernels.py:233-361): segment t
+ * of nsplit covers rows [t*ts/nsplit, (t+1)*ts/nsplit); each segment's partial
+ * is a serial sum from zero (zero when empty: _norm2_tail / _dot_seg :71-93),
+ * combined by `_pairwise_sum` (:191-199) -- ascending pairs, an odd tail
+ * carried.  nsplit == 1: the plain serial `_norm2_tail` / `_dot_tail`. */
+static inline C FN(split_dot)(const C *x, const C *y, int lo, int ts, int nsplit) {
+    if (nsplit <= 1) {
+        C s = (C)0;
+        for (int j = lo; j < ts; ++j) s += x[j] * y[j];
+        return s;
+    }
+    C v[128];
+    for (int t = 0; t < nsplit; ++t) {
+        int s0 = t * ts / nsplit, s1 = (t + 1) * ts / nsplit;
+        int l = lo > s0 ? lo : s0;
+        C s = (C)0;
+        for (int j = l; j < s1; ++j) s += x[j] * y[j];
+        v[t] = l < s1 ? s : (C)0;
+    }
+    int len = nsplit;
+    while (len > 1) {
+        int m = 0;
+        for (int j = 0; j + 1 < len; j += 2) v[m++] = v[j] + v[j + 1];
+        if (len & 1) v[m++] = v[len - 1];
+        len = m;
+    }
+    return v[0];
+}
+
+/* Split-K segment updates (kernels.py:134-141 `_geqrt_seg_update`, :159-166
+ * `_tsqrt_seg_update`) are njit functions the Python-level split-K generator
+ * calls with x and rho' as Python floats: numba specialises them for float64
+ * scalars, so for fp32 compute each element is updated in double and rounded
+ * once.  (Same value as the plain form in fp64.) */
+#define SEG_UPD(v, rhop, c, x) ((C)((double)(v) - (double)(rhop) * ((double)(c) / (double)(x))))
+#define SEG_DIV(v, x) ((C)((double)(v) / (double)(x)))
+
+
 /* Element (i, j) of a strided view: base[i*rs + j*cs] (matrix.py:93-154;
  * the lazy transpose is rs/cs swapped, never a copy). */
 #define AT(p, i, j, rs, cs) ((p)[(int64_t)(i) * (rs) + (int64_t)(j) * (cs)])
@@ -46,7 +84,7 @@ static inline void FN(reflector_scalars)(C piv, C sigma, C aik, C rho, C eps10, 
  * within a phase is irrelevant because items only share `col`/`nrm`.
  * Row k is written back at step k in the reference; every P[k, i] is final
  * after step k, so a single store at the end is the same bytes. */
-void FN(oracle_geqrt)(S *a, int64_t rs, int64_t cs, int ts, C *tau) {
+void FN(oracle_geqrt)(S *a, int64_t rs, int64_t cs, int ts, C *tau, int nsplit) {
     const C zero = (C)0, two = (C)2, eps10 = (C)10 * (C)EPS;
     C *P = (C *)malloc(sizeof(C) * ts * ts);
     C *col = (C *)malloc(sizeof(C) * ts);
@@ -56,16 +94,22 @@ void FN(oracle_geqrt)(S *a, int64_t rs, int64_t cs, int ts, C *tau) {
     for (int k = 0; k < ts - 1; ++k) {
         C *ak = P + k * ts;
         for (int j = 0; j < ts; ++j) col[j] = ak[j];
-        C nrm = zero;                                   /* _norm2_tail :71-76 */
-        for (int j = k + 1; j < ts; ++j) nrm += col[j] * col[j];
+        /* _norm2_tail :71-76 (split-K: nparts + _pairwise_sum, :252-265) */
+        C nrm = FN(split_dot)(col, col, k + 1, ts, nsplit);
         for (int i = k; i < ts; ++i) {
             C *ai = P + i * ts;
-            C rho = zero;                               /* _dot_tail :79-84 */
-            for (int j = k + 1; j < ts; ++j) rho += ai[j] * col[j];
+            C rho = FN(split_dot)(ai, col, k + 1, ts, nsplit);   /* _dot_tail :79-84 */
             C x, t, rhop;
             FN(reflector_scalars)(col[k], nrm, ai[k], rho, eps10, two, &x, &t, &rhop);
             ai[k] = ai[k] - rhop;
-            if (i > k) {
+            if (nsplit > 1) {
+                if (i > k) {
+                    for (int j = k + 1; j < ts; ++j) ai[j] = SEG_UPD(ai[j], rhop, col[j], x);
+                } else {
+                    for (int j = k + 1; j < ts; ++j) ai[j] = SEG_DIV(ai[j], x);
+                    tau[k] = t;
+                }
+            } else if (i > k) {
                 for (int j = k + 1; j < ts; ++j) ai[j] = ai[j] - rhop * (col[j] / x);
             } else {
                 for (int j = k + 1; j < ts; ++j) ai[j] = ai[j] / x;
@@ -81,8 +125,8 @@ void FN(oracle_geqrt)(S *a, int64_t rs, int64_t cs, int ts, C *tau) {
 /* kernels.py:286-313 `tsqrt_kernel` (+ `_tsqrt_item` :144-156): the [R; B_l]
  * chain with R resident (compute precision) across all tiles l. */
 void FN(oracle_tsqrt_chain)(S *r, int64_t rrs, int64_t rcs, S **bs, int64_t brs, int64_t bcs,
-                            C **taus, int nb, int ts) {
-    const C zero = (C)0, two = (C)2, eps10 = (C)10 * (C)EPS;
+                            C **taus, int nb, int ts, int nsplit) {
+    const C two = (C)2, eps10 = (C)10 * (C)EPS;
     C *R = (C *)malloc(sizeof(C) * ts * ts);
     C *B = (C *)malloc(sizeof(C) * ts * ts);
     C *bcol = (C *)malloc(sizeof(C) * ts);
@@ -95,17 +139,22 @@ void FN(oracle_tsqrt_chain)(S *r, int64_t rrs, int64_t rcs, S **bs, int64_t brs,
             for (int j = 0; j < ts; ++j) B[i * ts + j] = LD(AT(b, j, i, brs, bcs));
         for (int k = 0; k < ts; ++k) {
             for (int j = 0; j < ts; ++j) bcol[j] = B[k * ts + j];
-            C sigma = zero;
-            for (int j = 0; j < ts; ++j) sigma += bcol[j] * bcol[j];
+            C sigma = FN(split_dot)(bcol, bcol, 0, ts, nsplit);
             C rkk = R[k * ts + k];
             for (int i = k; i < ts; ++i) {
                 C *ri = R + i * ts, *bi = B + i * ts;
-                C rho = zero;
-                for (int j = 0; j < ts; ++j) rho += bi[j] * bcol[j];
+                C rho = FN(split_dot)(bi, bcol, 0, ts, nsplit);
                 C x, t, rhop;
                 FN(reflector_scalars)(rkk, sigma, ri[k], rho, eps10, two, &x, &t, &rhop);
                 ri[k] = ri[k] - rhop;
-                if (i > k) {
+                if (nsplit > 1) {
+                    if (i > k) {
+                        for (int j = 0; j < ts; ++j) bi[j] = SEG_UPD(bi[j], rhop, bcol[j], x);
+                    } else {
+                        for (int j = 0; j < ts; ++j) bi[j] = SEG_DIV(bi[j], x);
+                        tau[k] = t;
+                    }
+                } else if (i > k) {
                     for (int j = 0; j < ts; ++j) bi[j] = bi[j] - rhop * (bcol[j] / x);
                 } else {
                     for (int j = 0; j < ts; ++j) bi[j] = bi[j] / x;
@@ -183,7 +232,7 @@ void FN(oracle_tsmqr)(S *y, int64_t yrs, int64_t ycs, S **xs, int64_t xrs, int64
 /* bandreduce.py:31-88 `getsmqrt` (fused path) on a view of the padded
  * column-major n x n matrix `a`; lq selects the lazy transpose.
  * tau: compute-dtype TauStore, column slot(k,l,side) (matrix.py:184-215). */
-static void FN(oracle_getsmqrt)(S *a, int64_t n, C *tau, int k, int N, int ts, int lq) {
+static void FN(oracle_getsmqrt)(S *a, int64_t n, C *tau, int k, int N, int ts, int lq, int nsplit) {
     int64_t rs = lq ? n : 1, cs = lq ? 1 : n;      /* view (i,j) -> base */
     int side = lq ? 1 : 0;
     int top = lq ? k + 1 : k;
@@ -191,7 +240,7 @@ static void FN(oracle_getsmqrt)(S *a, int64_t n, C *tau, int k, int N, int ts, i
 #define TILE(tr, tc) (a + (int64_t)(tr) * ts * rs + (int64_t)(tc) * ts * cs)
 #define TAU(kk, ll) (tau + ((int64_t)side * N * N + (int64_t)(kk) * N + (ll)) * ts)
     S *diag = TILE(top, k);
-    FN(oracle_geqrt)(diag, rs, cs, ts, TAU(k, top));
+    FN(oracle_geqrt)(diag, rs, cs, ts, TAU(k, top), nsplit);
     int ntrail = N - 1 - k;
     S *top_slab = TILE(top, k + 1);
     if (ntrail > 0)
@@ -207,7 +256,7 @@ static void FN(oracle_getsmqrt)(S *a, int64_t n, C *tau, int k, int N, int ts, i
         body[idx] = TILE(l, k + 1);
         tc[idx] = TAU(k, l);
     }
-    FN(oracle_tsqrt_chain)(diag, rs, cs, vt, rs, cs, tc, nrows, ts);
+    FN(oracle_tsqrt_chain)(diag, rs, cs, vt, rs, cs, tc, nrows, ts, nsplit);
     if (ntrail > 0)
         FN(oracle_tsmqr)(top_slab, rs, cs, body, rs, cs, vt, rs, cs, tc, nrows, ntrail * ts, ts);
     free(vt); free(body); free(tc);
@@ -217,13 +266,13 @@ static void FN(oracle_getsmqrt)(S *a, int64_t n, C *tau, int k, int N, int ts, i
 
 /* bandreduce.py:91-120 `banddiag` + `_clear_outside_band`.  a: padded
  * column-major N*ts square; tau: ts x 2N^2 compute-dtype store (zeroed). */
-void FN(oracle_banddiag)(S *a, int N, int ts, C *tau) {
+void FN(oracle_banddiag)(S *a, int N, int ts, C *tau, int nsplit) {
     int64_t n = (int64_t)N * ts;
     for (int k = 0; k < N - 1; ++k) {
-        FN(oracle_getsmqrt)(a, n, tau, k, N, ts, 0);
-        FN(oracle_getsmqrt)(a, n, tau, k, N, ts, 1);
+        FN(oracle_getsmqrt)(a, n, tau, k, N, ts, 0, nsplit);
+        FN(oracle_getsmqrt)(a, n, tau, k, N, ts, 1, nsplit);
     }
-    FN(oracle_getsmqrt)(a, n, tau, N - 1, N, ts, 0);
+    FN(oracle_getsmqrt)(a, n, tau, N - 1, N, ts, 0, nsplit);
     for (int64_t r = 0; r < n; ++r) {
         for (int64_t c = 0; c < r; ++c) a[c * n + r] = ST((C)0);
         for (int64_t c = r + ts + 1; c < n; ++c) a[c * n + r] = ST((C)0);

@@ -26,7 +26,7 @@ EXPORTS = (
     "bsvd_last_error", "bsvd_version", "bsvd_workspace_bytes", "bsvd_svdvals",
     "bsvd_svdvals_ex", "bsvd_svdvals_batched", "bsvd_banddiag",
     "bsvd_band_workspace_bytes", "bsvd_band_to_bidiagonal", "bsvd_bidiagonal_values", "bsvd_geqrt",
-    "bsvd_tsqrt_chain", "bsvd_unmqr", "bsvd_tsmqr_fused", "bsvd_launch_counter",
+    "bsvd_tsqrt_chain", "bsvd_geqrt_splitk", "bsvd_tsqrt_chain_splitk", "bsvd_unmqr", "bsvd_tsmqr_fused", "bsvd_launch_counter",
 )
 
 
@@ -76,6 +76,8 @@ def load(path: str = LIB_PATH):
         "bsvd_bidiagonal_values": (i32, [dp, dp, i64, dp, vp]),
         "bsvd_geqrt": (i32, [vp, i64, i64, i32, i32, vp, vp]),
         "bsvd_tsqrt_chain": (i32, [vp, i64, i64, vp, vp, i32, i32, i32, vp]),
+        "bsvd_geqrt_splitk": (i32, [vp, i64, i64, i32, i32, i32, vp, vp]),
+        "bsvd_tsqrt_chain_splitk": (i32, [vp, i64, i64, vp, vp, i32, i32, i32, i32, vp]),
         "bsvd_unmqr": (i32, [vp, i64, i64, vp, vp, i64, i64, i64, i32, i32, i32, vp]),
         "bsvd_tsmqr_fused": (i32, [vp, i64, i64, vp, vp, vp, i32, i64, i32, i32, i32, vp]),
     }

@@ -7,7 +7,8 @@ pipeline (``stage1="tree"`` fast path or ``"faithful"`` reference-exact
 stage 1).  Its ``launch`` is a kernel-level registry: the reference's tile
 kernels (``geqrt_kernel``, ``tsqrt_kernel``, ``unmqr_kernel``,
 ``tsmqr_kernel``, kernels.py:205-421) run as their bit-faithful sm_100a
-counterparts, so the reference's own driver (``bandsvd.banddiag`` /
+counterparts (``geqrt_splitk_kernel`` / ``tsqrt_splitk_kernel`` included,
+kernels.py:233-361), so the reference's own driver (``bandsvd.banddiag`` /
 ``bandsvd.svdvals``) can execute stage 1 on the B200 unchanged.
 """
 from __future__ import annotations
@@ -128,15 +129,21 @@ class B200Backend:
         def back(t, arr):
             arr[...] = t.cpu().numpy().T
 
-        if name == "geqrt_kernel":
+        if name in ("geqrt_kernel", "geqrt_splitk_kernel"):
+            # geqrt_kernel(ctx, a, tau, ...) / geqrt_splitk_kernel(ctx, a, tau, nsplit, ...)
             a, tau = args[0], args[1]
             ts = a.shape[0]
             ta, _ = dev(a)
             tt = torch.from_numpy(np.array(tau)).to(self.device)
-            _lib.check(L.bsvd_geqrt(ta.data_ptr(), 1, ts, _DT_CODE[a.dtype], ts, tt.data_ptr(), st))
+            if name == "geqrt_kernel":
+                _lib.check(L.bsvd_geqrt(ta.data_ptr(), 1, ts, _DT_CODE[a.dtype], ts, tt.data_ptr(), st))
+            else:
+                _lib.check(L.bsvd_geqrt_splitk(ta.data_ptr(), 1, ts, _DT_CODE[a.dtype], ts, int(args[2]),
+                                               tt.data_ptr(), st))
             back(ta, a)
             tau[...] = tt.cpu().numpy()
-        elif name == "tsqrt_kernel":
+        elif name in ("tsqrt_kernel", "tsqrt_splitk_kernel"):
+            # tsqrt_kernel(ctx, r, bs, taus, ...) / tsqrt_splitk_kernel(ctx, r, bs, taus, nsplit, ...)
             r, bs, taus = args[0], args[1], args[2]
             ts = r.shape[0]
             tr, _ = dev(r)
@@ -144,8 +151,12 @@ class B200Backend:
             ttau = [torch.from_numpy(np.array(t)).to(self.device) for t in taus]
             pb = torch.tensor([t.data_ptr() for t in tbs], dtype=torch.int64, device=self.device)
             pt = torch.tensor([t.data_ptr() for t in ttau], dtype=torch.int64, device=self.device)
-            _lib.check(L.bsvd_tsqrt_chain(tr.data_ptr(), 1, ts, pb.data_ptr(), pt.data_ptr(),
-                                          len(bs), _DT_CODE[r.dtype], ts, st))
+            if name == "tsqrt_kernel":
+                _lib.check(L.bsvd_tsqrt_chain(tr.data_ptr(), 1, ts, pb.data_ptr(), pt.data_ptr(),
+                                              len(bs), _DT_CODE[r.dtype], ts, st))
+            else:
+                _lib.check(L.bsvd_tsqrt_chain_splitk(tr.data_ptr(), 1, ts, pb.data_ptr(), pt.data_ptr(),
+                                                     len(bs), _DT_CODE[r.dtype], ts, int(args[3]), st))
             back(tr, r)
             for t, b in zip(tbs, bs):
                 back(t, b)
@@ -176,8 +187,7 @@ class B200Backend:
             for t, x in zip(txs, xs):
                 back(t, x)
         else:
-            raise ConfigError(f"B200Backend has no sm_100a kernel for {name!r} "
-                              "(split-K panels are served by the fused stage-1 pipeline)")
+            raise ConfigError(f"B200Backend has no sm_100a kernel for {name!r}")
         self.cuda_stream().synchronize()
         self.stats.launches += 1
         return self.stats.delta_since(before)

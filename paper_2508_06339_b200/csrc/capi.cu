@@ -116,7 +116,7 @@ bsvd_status stage1(S *work, const Plan &p, const bsvd_config &c, int algo, char 
         C *tau = (C *)scratch;
         for (int64_t b = 0; b < p.batch; ++b) {
             BSVD_CUDA_TRY(cudaMemsetAsync(tau, 0, (size_t)p.ts * 2 * p.N * p.N * sizeof(C), st));
-            e = banddiag_faithful<S, C>(work + b * p.np * p.np, p.np, p.ts, c.colperblock, tau, st);
+            e = banddiag_faithful<S, C>(work + b * p.np * p.np, p.np, p.ts, c.colperblock, tau, st, c.splitk);
             if (e != cudaSuccess) return cuda_error(e, "stage 1 (faithful)");
         }
         return BSVD_OK;
@@ -416,6 +416,43 @@ bsvd_status bsvd_tsqrt_chain(void *r, int64_t rs, int64_t cs, void *const *b_til
               (launch_tsqrt_faithful<float, float>((float *)r, rs, cs, bs, ta, nb, ts, st)),
               (launch_tsqrt_faithful<__half, float>((__half *)r, rs, cs, bs, ta, nb, ts, st)));
     if (err != cudaSuccess) return cuda_error(err, "tsqrt_chain");
+    return BSVD_OK;
+}
+
+static bsvd_status check_splitk(int32_t ts, int32_t nsplit) {
+    const int kmax = std::min((int)ts, 1024 / (int)ts);
+    if (nsplit < 1 || nsplit > kmax)
+        return set_error(BSVD_E_CONFIG,
+                         "splitk must lie in [1, min(TILESIZE, 1024/TILESIZE)] = [1, %d], got %d", kmax, nsplit);
+    return BSVD_OK;
+}
+
+bsvd_status bsvd_geqrt_splitk(void *tile, int64_t rs, int64_t cs, bsvd_dtype dtype, int32_t ts, int32_t splitk,
+                              void *tau, void *stream) {
+    if (ts < 4 || ts > 128) return set_error(BSVD_E_CONFIG, "tilesize must be an integer in [4, 128], got %d", ts);
+    if (bsvd_status s = check_splitk(ts, splitk)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t err;
+    DISPATCH3(dtype,
+              (launch_geqrt_faithful<double, double>((double *)tile, rs, cs, ts, (double *)tau, 1, 0, 0, st, splitk)),
+              (launch_geqrt_faithful<float, float>((float *)tile, rs, cs, ts, (float *)tau, 1, 0, 0, st, splitk)),
+              (launch_geqrt_faithful<__half, float>((__half *)tile, rs, cs, ts, (float *)tau, 1, 0, 0, st, splitk)));
+    if (err != cudaSuccess) return cuda_error(err, "geqrt_splitk");
+    return BSVD_OK;
+}
+
+bsvd_status bsvd_tsqrt_chain_splitk(void *r, int64_t rs, int64_t cs, void *const *b_tiles, void *const *taus,
+                                    int32_t nb, bsvd_dtype dtype, int32_t ts, int32_t splitk, void *stream) {
+    if (ts < 4 || ts > 128) return set_error(BSVD_E_CONFIG, "tilesize must be an integer in [4, 128], got %d", ts);
+    if (bsvd_status s = check_splitk(ts, splitk)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    TileArr bs{b_tiles}, ta{taus};
+    cudaError_t err;
+    DISPATCH3(dtype,
+              (launch_tsqrt_faithful<double, double>((double *)r, rs, cs, bs, ta, nb, ts, st, splitk)),
+              (launch_tsqrt_faithful<float, float>((float *)r, rs, cs, bs, ta, nb, ts, st, splitk)),
+              (launch_tsqrt_faithful<__half, float>((__half *)r, rs, cs, bs, ta, nb, ts, st, splitk)));
+    if (err != cudaSuccess) return cuda_error(err, "tsqrt_chain_splitk");
     return BSVD_OK;
 }
 

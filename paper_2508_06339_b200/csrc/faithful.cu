@@ -15,13 +15,64 @@
 namespace bsvd {
 
 constexpr int kMaxTs = 128;
+constexpr int kMaxSplit = 32;   // splitk <= min(ts, 1024 / ts) (kernels.py:52)
+
+// Split-K segment updates (kernels.py:134-141 _geqrt_seg_update, :159-166
+// _tsqrt_seg_update) are njit functions called from the Python-level split-K
+// generator with x and rho' as Python floats, so numba specialises them for
+// float64 scalars: for fp32 compute every updated element is
+// float32(double(v) - double(rho') * (double(col) / double(x))) (resp.
+// float32(double(v) / double(x))) -- one rounding instead of three.  For fp64
+// the two forms coincide.  (The pivot-row element pivots[i] - rho' is numpy
+// float32 - Python float, float32 arithmetic under NEP 50.)
+template <typename C>
+__device__ __forceinline__ C seg_upd(C v, C rhop, C c, C x) {
+    return (C)((double)v - (double)rhop * ((double)c / (double)x));
+}
+template <typename C>
+__device__ __forceinline__ C seg_div(C v, C x) {
+    return (C)((double)v / (double)x);
+}
+
+// Split-K sums (kernels.py:233-283, :316-361): segment t of nsplit covers rows
+// [t*ts/nsplit, (t+1)*ts/nsplit); each segment's partial is a serial sum from
+// zero over its rows in [lo, ts) (zero when empty: _norm2_tail / _dot_seg
+// :71-93), then _pairwise_sum (:191-199) combines the partials pairwise in
+// ascending index, an odd tail carried to the next round.  nsplit == 1 is
+// the plain serial sum of geqrt_kernel / tsqrt_kernel.
+template <typename C, typename F>
+__device__ __forceinline__ C split_sum(int ts, int nsplit, int lo, F term) {
+    if (nsplit <= 1) {
+        C s = C(0);
+        for (int j = lo; j < ts; ++j) s += term(j);
+        return s;
+    }
+    C v[kMaxSplit];
+    for (int t = 0; t < nsplit; ++t) {
+        const int s0 = t * ts / nsplit, s1 = (t + 1) * ts / nsplit;
+        const int l = lo > s0 ? lo : s0;
+        C s = C(0);
+        for (int j = l; j < s1; ++j) s += term(j);
+        v[t] = l < s1 ? s : C(0);
+    }
+    int len = nsplit;
+    while (len > 1) {
+        int m = 0;
+        for (int j = 0; j + 1 < len; j += 2) v[m++] = v[j] + v[j + 1];
+        if (len & 1) v[m++] = v[len - 1];
+        len = m;
+    }
+    return v[0];
+}
 
 // kernels.py:205-230 geqrt_kernel (+ _geqrt_item :119-131, _norm2_tail :71-76,
-// _dot_tail :79-84).  ts threads, one tile per CTA (blockIdx.y = batch).
+// _dot_tail :79-84); nsplit > 1: geqrt_splitk_kernel :233-283, whose only
+// arithmetic difference is the split-K order of the norm and dot sums
+// (split_sum).  ts threads, one tile per CTA (blockIdx.y = batch).
 template <typename S, typename C>
 __global__ void __launch_bounds__(kMaxTs) k_geqrt_faithful(S *a, int64_t rs, int64_t cs,
                                                            int64_t a_bstride, int ts, C *tau,
-                                                           int64_t tau_bstride) {
+                                                           int64_t tau_bstride, int nsplit) {
     using CV = Conv<S, C>;
     __shared__ C col[kMaxTs];
     __shared__ C nrm;
@@ -34,19 +85,23 @@ __global__ void __launch_bounds__(kMaxTs) k_geqrt_faithful(S *a, int64_t rs, int
     C tau_i = zero;
     for (int k = 0; k < ts - 1; ++k) {
         if (i == k) {
-            C s = zero;
             for (int j = 0; j < ts; ++j) col[j] = ai[j];
-            for (int j = k + 1; j < ts; ++j) s += ai[j] * ai[j];
-            nrm = s;
+            nrm = split_sum<C>(ts, nsplit, k + 1, [&](int j) { return ai[j] * ai[j]; });
         }
         __syncthreads();
         if (i >= k) {
-            C rho = zero;
-            for (int j = k + 1; j < ts; ++j) rho += ai[j] * col[j];
+            const C rho = split_sum<C>(ts, nsplit, k + 1, [&](int j) { return ai[j] * col[j]; });
             C x, t, rhop;
             reflector_scalars(col[k], nrm, ai[k], rho, eps10, two, x, t, rhop);
             ai[k] = ai[k] - rhop;
-            if (i > k) {
+            if (nsplit > 1) {
+                if (i > k) {
+                    for (int j = k + 1; j < ts; ++j) ai[j] = seg_upd(ai[j], rhop, col[j], x);
+                } else {
+                    for (int j = k + 1; j < ts; ++j) ai[j] = seg_div(ai[j], x);
+                    tau_i = t;
+                }
+            } else if (i > k) {
                 for (int j = k + 1; j < ts; ++j) ai[j] = ai[j] - rhop * (col[j] / x);
             } else {
                 for (int j = k + 1; j < ts; ++j) ai[j] = ai[j] / x;
@@ -61,11 +116,12 @@ __global__ void __launch_bounds__(kMaxTs) k_geqrt_faithful(S *a, int64_t rs, int
 }
 
 // kernels.py:286-313 tsqrt_kernel (+ _tsqrt_item :144-156): the [R; B_l]
-// chain, R columns resident in the work-items across all l.
+// chain, R columns resident in the work-items across all l; nsplit > 1:
+// tsqrt_splitk_kernel :316-361 (split-K norm / dot order, split_sum).
 template <typename S, typename C, typename TileSeqT, typename TauSeqT>
 __global__ void __launch_bounds__(kMaxTs) k_tsqrt_faithful(S *r, int64_t rs, int64_t cs,
                                                            TileSeqT bs, TauSeqT taus, int nb,
-                                                           int ts) {
+                                                           int ts, int nsplit) {
     using CV = Conv<S, C>;
     __shared__ C bcol[kMaxTs];
     __shared__ C scal[2];
@@ -80,20 +136,24 @@ __global__ void __launch_bounds__(kMaxTs) k_tsqrt_faithful(S *r, int64_t rs, int
         C tau_i = zero;
         for (int k = 0; k < ts; ++k) {
             if (i == k) {
-                C s = zero;
                 for (int j = 0; j < ts; ++j) bcol[j] = bi[j];
-                for (int j = 0; j < ts; ++j) s += bi[j] * bi[j];
-                scal[0] = s;
+                scal[0] = split_sum<C>(ts, nsplit, 0, [&](int j) { return bi[j] * bi[j]; });
                 scal[1] = ri[k];
             }
             __syncthreads();
             if (i >= k) {
-                C rho = zero;
-                for (int j = 0; j < ts; ++j) rho += bi[j] * bcol[j];
+                const C rho = split_sum<C>(ts, nsplit, 0, [&](int j) { return bi[j] * bcol[j]; });
                 C x, t, rhop;
                 reflector_scalars(scal[1], scal[0], ri[k], rho, eps10, two, x, t, rhop);
                 ri[k] = ri[k] - rhop;
-                if (i > k) {
+                if (nsplit > 1) {
+                    if (i > k) {
+                        for (int j = 0; j < ts; ++j) bi[j] = seg_upd(bi[j], rhop, bcol[j], x);
+                    } else {
+                        for (int j = 0; j < ts; ++j) bi[j] = seg_div(bi[j], x);
+                        tau_i = t;
+                    }
+                } else if (i > k) {
                     for (int j = 0; j < ts; ++j) bi[j] = bi[j] - rhop * (bcol[j] / x);
                 } else {
                     for (int j = 0; j < ts; ++j) bi[j] = bi[j] / x;
@@ -177,18 +237,18 @@ __global__ void __launch_bounds__(kMaxTs) k_tsmqr_faithful(S *y, int64_t rs, int
 
 template <typename S, typename C>
 cudaError_t launch_geqrt_faithful(S *a, int64_t rs, int64_t cs, int ts, C *tau, int64_t batch,
-                                  int64_t a_bstride, int64_t tau_bstride, cudaStream_t st) {
+                                  int64_t a_bstride, int64_t tau_bstride, cudaStream_t st, int nsplit) {
     k_geqrt_faithful<S, C><<<dim3(1, (unsigned)batch), ts, 0, st>>>(a, rs, cs, a_bstride, ts, tau,
-                                                                    tau_bstride);
+                                                                    tau_bstride, nsplit);
     bsvd_host::count_launch();
     return cudaGetLastError();
 }
 
 template <typename S, typename C, typename TS_, typename TA_>
 cudaError_t launch_tsqrt_faithful(S *r, int64_t rs, int64_t cs, TS_ bs, TA_ taus, int nb, int ts,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, int nsplit) {
     if (nb <= 0) return cudaSuccess;
-    k_tsqrt_faithful<S, C, TS_, TA_><<<1, ts, 0, st>>>(r, rs, cs, bs, taus, nb, ts);
+    k_tsqrt_faithful<S, C, TS_, TA_><<<1, ts, 0, st>>>(r, rs, cs, bs, taus, nb, ts, nsplit);
     bsvd_host::count_launch();
     return cudaGetLastError();
 }
@@ -217,7 +277,7 @@ cudaError_t launch_tsmqr_faithful(S *y, int64_t rs, int64_t cs, TS_ xs, TS_ vs, 
 // bandreduce.py:31-88 getsmqrt (fused) + :91-120 banddiag, faithful order.
 // a: padded column-major n x n (n = N*ts); tau: ts x 2N^2 compute-dtype store.
 template <typename S, typename C>
-cudaError_t banddiag_faithful(S *a, int64_t n, int ts, int cpb, C *tau, cudaStream_t st) {
+cudaError_t banddiag_faithful(S *a, int64_t n, int ts, int cpb, C *tau, cudaStream_t st, int splitk) {
     const int N = (int)(n / ts);
     auto sweep = [&](int k, bool lq) -> cudaError_t {
         const int64_t rs = lq ? n : 1, cs = lq ? 1 : n;
@@ -229,7 +289,7 @@ cudaError_t banddiag_faithful(S *a, int64_t n, int ts, int cpb, C *tau, cudaStre
             return tau + ((int64_t)side * N * N + (int64_t)kk * N + ll) * ts;
         };
         S *diag = tile(top, k);
-        cudaError_t e = launch_geqrt_faithful<S, C>(diag, rs, cs, ts, tauc(k, top), 1, 0, 0, st);
+        cudaError_t e = launch_geqrt_faithful<S, C>(diag, rs, cs, ts, tauc(k, top), 1, 0, 0, st, splitk);
         if (e != cudaSuccess) return e;
         const int ntrail = N - 1 - k;
         S *top_slab = tile(top, k + 1);
@@ -244,7 +304,7 @@ cudaError_t banddiag_faithful(S *a, int64_t n, int ts, int cpb, C *tau, cudaStre
         TileSeq vts{(char *)tile(top + 1, k), tstep};
         TileSeq body{(char *)tile(top + 1, k + 1), tstep};
         TileSeq tcs{(char *)tauc(k, top + 1), (int64_t)ts * (int64_t)sizeof(C)};
-        e = launch_tsqrt_faithful<S, C>(diag, rs, cs, vts, tcs, nrows, ts, st);
+        e = launch_tsqrt_faithful<S, C>(diag, rs, cs, vts, tcs, nrows, ts, st, splitk);
         if (e != cudaSuccess) return e;
         if (ntrail > 0)
             e = launch_tsmqr_faithful<S, C>(top_slab, rs, cs, body, vts, tcs, nrows,
@@ -262,15 +322,15 @@ cudaError_t banddiag_faithful(S *a, int64_t n, int ts, int cpb, C *tau, cudaStre
 
 #define INST(S, C)                                                                              \
     template cudaError_t launch_geqrt_faithful<S, C>(S *, int64_t, int64_t, int, C *, int64_t,   \
-                                                     int64_t, int64_t, cudaStream_t);            \
+                                                     int64_t, int64_t, cudaStream_t, int);       \
     template cudaError_t launch_tsqrt_faithful<S, C, TileArr, TileArr>(                          \
-        S *, int64_t, int64_t, TileArr, TileArr, int, int, cudaStream_t);                        \
+        S *, int64_t, int64_t, TileArr, TileArr, int, int, cudaStream_t, int);                   \
     template cudaError_t launch_unmqr_faithful<S, C>(const S *, int64_t, int64_t, const C *, S *, \
                                                      int64_t, int64_t, int64_t, int, int,         \
                                                      cudaStream_t);                              \
     template cudaError_t launch_tsmqr_faithful<S, C, TileArr, TileArr>(                          \
         S *, int64_t, int64_t, TileArr, TileArr, TileArr, int, int64_t, int, int, cudaStream_t);  \
-    template cudaError_t banddiag_faithful<S, C>(S *, int64_t, int, int, C *, cudaStream_t);
+    template cudaError_t banddiag_faithful<S, C>(S *, int64_t, int, int, C *, cudaStream_t, int);
 INST(double, double)
 INST(float, float)
 INST(__half, float)

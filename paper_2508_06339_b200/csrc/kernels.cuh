@@ -18,10 +18,10 @@ struct TileArr {
 // ---- faithful.cu (bit-exact reference kernels) ---------------------------
 template <typename S, typename C>
 cudaError_t launch_geqrt_faithful(S *a, int64_t rs, int64_t cs, int ts, C *tau, int64_t batch,
-                                  int64_t a_bstride, int64_t tau_bstride, cudaStream_t st);
+                                  int64_t a_bstride, int64_t tau_bstride, cudaStream_t st, int nsplit = 1);
 template <typename S, typename C, typename TS_, typename TA_>
 cudaError_t launch_tsqrt_faithful(S *r, int64_t rs, int64_t cs, TS_ bs, TA_ taus, int nb, int ts,
-                                  cudaStream_t st);
+                                  cudaStream_t st, int nsplit = 1);
 template <typename S, typename C>
 cudaError_t launch_unmqr_faithful(const S *panel, int64_t prs, int64_t pcs, const C *tau, S *x,
                                   int64_t xrs, int64_t xcs, int64_t ncols, int ts, int cpb,
@@ -30,7 +30,7 @@ template <typename S, typename C, typename TS_, typename TA_>
 cudaError_t launch_tsmqr_faithful(S *y, int64_t rs, int64_t cs, TS_ xs, TS_ vs, TA_ taus, int nb,
                                   int64_t ncols, int ts, int cpb, cudaStream_t st);
 template <typename S, typename C>
-cudaError_t banddiag_faithful(S *a, int64_t n, int ts, int cpb, C *tau, cudaStream_t st);
+cudaError_t banddiag_faithful(S *a, int64_t n, int ts, int cpb, C *tau, cudaStream_t st, int splitk = 1);
 
 // ---- stage1_tree.cu (fast stage 1) ---------------------------------------
 // Workspace bytes for one matrix of padded order n with tile ts.

@@ -327,3 +327,66 @@ def test_backend_on_side_stream(P, oracle):
     vals = got.cpu().numpy()                    # read on the current stream
     want = 2.0 * oracle.svdvals(x.cpu().numpy().T.copy(), 64)
     assert_close(vals, want, np.float32, 1024, what="side stream")
+
+
+# ---- split-K panels: faithful kernels and stage 1 bit-identical -----------
+
+@pytest.mark.parametrize("name", golden_names("splitk_geqrt_"))
+def test_geqrt_splitk_kernel_bitwise(P, be_tree, name):
+    g = load_golden(name)
+    tile = np.asfortranarray(g["a"].copy())
+    tau = np.zeros(tile.shape[0], g["tau"].dtype)
+    be_tree.launch(_K("geqrt_splitk_kernel"), None, (tile, tau, int(g["splitk"]), None, None, None))
+    assert same_bits(tile, np.asfortranarray(g["out"]))
+    assert same_bits(tau, g["tau"])
+
+
+@pytest.mark.parametrize("name", golden_names("splitk_pipe_"))
+def test_faithful_band_splitk_bitwise(P, be_faithful, name):
+    g = load_golden(name)
+    cfg = P.KernelConfig(tilesize=int(g["ts"]), splitk=int(g["splitk"]))
+    band = P.banddiag(g["a"], cfg, backend=be_faithful)
+    assert same_bits(np.asfortranarray(band), np.asfortranarray(g["band"]))
+    vals = P.svdvals(g["a"], cfg, backend=be_faithful)
+    assert_close(vals, g["vals"], g["a"].dtype, g["a"].shape[0], what=name)
+
+
+def _reference_package():
+    """The unmodified reference installed under baseline/_ref (pip --target,
+    git-ignored; travels to the GPU box) or None."""
+    import importlib
+    import os
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "bandsvd")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        return importlib.import_module("bandsvd")
+    except Exception:
+        return None
+
+
+@pytest.mark.parametrize("name,splitk", [("pipe_float32_n64_ts16", 1), ("pipe_float64_n96_ts32", 1),
+                                         ("splitk_pipe_float64_n64_ts16_k3", 3),
+                                         ("splitk_pipe_float16_n40_ts8_k2", 2)])
+def test_reference_driver_on_b200_backend(P, be_faithful, name, splitk):
+    """The reference's OWN stage-1 driver (bandsvd.banddiag -> getsmqrt ->
+    geqrt / unmqr / tsqrt_chain / tsmqr_fused launches, bandreduce.py:31-120)
+    with a B200Backend plugged in: every tile kernel runs on the GPU through
+    B200Backend.launch, and the band is the reference's bytes."""
+    B = _reference_package()
+    if B is None:
+        pytest.skip("reference not installed under baseline/_ref")
+    g = load_golden(name)
+    ts = int(g["ts"])
+    m = B.DenseMatrix.from_array(g["a"])
+    pm = B.matrix.pad_to_tiles(m, ts)
+    N = pm.rows // ts
+    work = pm.copy()
+    tau = B.TauStore(ts, N, m.precision.compute_dtype)
+    before = be_faithful.stats.launches
+    B.banddiag(work, tau, N, B.KernelConfig(tilesize=ts, splitk=splitk), be_faithful)
+    assert be_faithful.stats.launches > before
+    assert same_bits(np.asfortranarray(work.array), np.asfortranarray(g["band"]))
