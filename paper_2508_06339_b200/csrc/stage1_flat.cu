@@ -1284,7 +1284,7 @@ template <typename S, int TS, bool CM>
 __global__ void __launch_bounds__(kGT, 1)
 k_fgemm1(const S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *ws0,
          int64_t ws_bstride, int64_t n, int nsplit, int rps, int par) {
-    constexpr int BM = TS, BN = 128;
+    constexpr int BM = TS < 64 ? 64 : TS, BN = 128;   // ts = 32: rows >= TS zero-filled, masked
     using TL = Tile<BM, BN>;
     __shared__ __align__(16) float As[2][TL::A_EL];
     __shared__ __align__(16) float Bs[2][TL::B_EL];
@@ -1336,11 +1336,11 @@ template <typename S, int TS, bool CM>
 __global__ void __launch_bounds__(kGT, 1)
 k_fw2x1(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *ws0, int64_t ws_bstride,
         int64_t n, int nsplit, int nused, int par, int w2t) {
-    constexpr int BM = TS, BN = 64;
+    constexpr int BM = TS < 64 ? 64 : TS, BN = 64;    // ts = 32: rows >= TS zero-filled, masked
     using TL = Tile<BM, BN>;
     __shared__ __align__(16) float As[2][TL::A_EL];
     __shared__ __align__(16) float Bs[2][TL::B_EL];
-    extern __shared__ __align__(16) float W2s[];   // [TS][BNP]
+    extern __shared__ __align__(16) float W2s[];   // [BM][BNP]
     const int b = blockIdx.z;
     X += (int64_t)b * a_bstride;
     const Ws w = ws_carve(ws0 + (int64_t)b * ws_bstride, n, TS, nsplit);
@@ -1385,7 +1385,7 @@ k_fw2x1(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *w
             const int c = TL::col(tn, h * 4);
             const float4 v = make_float4(acc[ii][h * 4], acc[ii][h * 4 + 1], acc[ii][h * 4 + 2], acc[ii][h * 4 + 3]);
             *reinterpret_cast<float4 *>(&W2s[r * TL::BNP + c]) = v;
-            if (c0 + c < C) {
+            if (c0 + c < C && r < TS) {
                 *reinterpret_cast<float4 *>(&w.W2[(int64_t)r * C + c0 + c]) = v;
                 if (w2t) {   // K-major copy for the tensor-core update: W2T[c][j]
                     float *t = w.W2T + (int64_t)(c0 + c) * TS + r;
@@ -1415,7 +1415,7 @@ k_fw2x1(S *__restrict__ X, int64_t ld, int64_t a_bstride, int M, int C, float *w
 template <int TS>
 __global__ void __launch_bounds__(kGT, 1)
 k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps, int par) {
-    constexpr int BM = TS, BN = TS;
+    constexpr int BM = TS < 64 ? 64 : TS, BN = BM;    // ts = 32: zero-filled beyond TS, masked
     using TL = Tile<BM, BN>;
     __shared__ __align__(16) float As[2][TL::A_EL];
     __shared__ __align__(16) float Bs[2][TL::B_EL];
@@ -1684,16 +1684,17 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
     if (e != cudaSuccess) return e;
     const int64_t N = n / TS;
     const int nsplit = nsplit_for(batch);
+    constexpr int W2BM = TS < 64 ? 64 : TS;   // k_fw2x1's tile rows
     const int64_t wsb = (int64_t)ws_floats(n, TS, nsplit);
     cudaStream_t sp = cx->sp, su = cx->su;
     cudaEvent_t evStart = cx->ev[0], evP = cx->ev[1], ev1 = cx->ev[2], evW = cx->ev[3], evEndP = cx->ev[4],
                 evEndU = cx->ev[5];
     {   // (function attributes are per device: set before every stage)
         e = cudaFuncSetAttribute(k_fw2x1<S, TS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(TS * (64 + 4) * sizeof(float)));
+                                 (int)(W2BM * (64 + 4) * sizeof(float)));
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(k_fw2x1<S, TS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(TS * (64 + 4) * sizeof(float)));
+                                 (int)(W2BM * (64 + 4) * sizeof(float)));
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(k_fgram<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)((TS * (TS + 1) + TS * TS / 4) * sizeof(float)));
@@ -1816,7 +1817,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
             if (e2 != cudaSuccess) return e2;
             cudaEventRecord(ev1, su);
             cudaStreamWaitEvent(sp, ev1, 0);
-            const size_t w2sm = TS * (64 + 4) * sizeof(float);
+            const size_t w2sm = W2BM * (64 + 4) * sizeof(float);
             if (lq)
                 k_fw2x1<S, TS, false><<<dim3((unsigned)((C + 63) / 64), 1, (unsigned)batch), kGT, w2sm, sp>>>(
                     X, rs, a_bstride, M, C, ws, wsb, n, nsplit, ns, par, tc2 ? 1 : 0);
@@ -1880,7 +1881,7 @@ bool flat_supported(int ts, int elem_bytes) {
     if (const char *s = getenv("BSVD_FLAT")) {
         if (atoi(s) == 0) return false;
     }
-    return (ts == 64 || ts == 128) && elem_bytes <= 4;
+    return (ts == 32 || ts == 64 || ts == 128) && elem_bytes <= 4;
 }
 
 template <typename S>
@@ -1888,7 +1889,8 @@ cudaError_t banddiag_flat(S *a, int64_t n, int ts, int64_t batch, int64_t a_bstr
                           double *panel_ms, double *trail_ms) {
     const bool timed = panel_ms != nullptr;
     if (ts == 128) return flat::run_flat<S, 128>(a, n, batch, a_bstride, (float *)ws, st, panel_ms, trail_ms, timed);
-    return flat::run_flat<S, 64>(a, n, batch, a_bstride, (float *)ws, st, panel_ms, trail_ms, timed);
+    if (ts == 64) return flat::run_flat<S, 64>(a, n, batch, a_bstride, (float *)ws, st, panel_ms, trail_ms, timed);
+    return flat::run_flat<S, 32>(a, n, batch, a_bstride, (float *)ws, st, panel_ms, trail_ms, timed);
 }
 
 template cudaError_t banddiag_flat<float>(float *, int64_t, int, int64_t, int64_t, void *, cudaStream_t, double *, double *);

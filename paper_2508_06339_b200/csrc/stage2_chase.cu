@@ -1089,9 +1089,19 @@ __global__ void __launch_bounds__(NW * 32) k_chase_cta(T *band, int64_t n, int b
 // the carried-block chase
 static int chase_max_ops(int64_t n, int b) { return 3 + (int)(2 * ((n + b - 1) / b)); }
 
+// k_chase2 serves every band width of single matrices and small batches
+// (narrow bands too: measured 2-2.7x faster than the first-generation
+// pipelined k_chase at b = 32 / 64, n = 300..2048); batches of >= 512 narrow
+// bands keep one CTA per matrix (k_chase_cta).  BSVD_CHASE2_MIN=b restricts
+// it to wider bands (development knob).
+static bool chase2_used(int b, int64_t batch) {
+    static const int lo = getenv("BSVD_CHASE2_MIN") ? atoi(getenv("BSVD_CHASE2_MIN")) : 0;
+    return b > lo && b <= ch2::BK && (b > 64 || batch < 512);
+}
+
 size_t chase_workspace_bytes(int64_t n, int bw, int64_t batch) {
     const int64_t ld = 3 * (int64_t)bw + 1;
-    size_t flags = bw > 64 ? (size_t)batch * n * chase_max_ops(n, bw) * sizeof(int) : 0;
+    size_t flags = chase2_used(bw, batch) ? (size_t)batch * n * chase_max_ops(n, bw) * sizeof(int) : 0;
     return (size_t)batch * (size_t)n * ((size_t)ld * sizeof(double) + sizeof(int)) + flags + 512;
 }
 
@@ -1167,7 +1177,7 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
     if (n < 1 || batch < 1) return cudaSuccess;
     const int b = bw;
     const int64_t ld = 3 * (int64_t)b + 1;
-    if (n > 2 && b > 64 && b <= ch2::BK && !getenv("BSVD_CHASE_V1")) {
+    if (n > 2 && chase2_used(b, batch) && !getenv("BSVD_CHASE_V1")) {
         // carried-block cluster chase, in the compute precision of the input
         // (fp32 for FP32 / FP16 storage like the reference's chase,
         // secondstage.py:456-457; BSVD_CHASE_F64=1 keeps fp64)
