@@ -196,8 +196,8 @@ def banddiag(a, cfg: KernelConfig | None = None, backend=None):
     """Stage 1 only: reduce a square matrix (zero-padded to a multiple of
     cfg.tilesize) to upper-band form, band width = tilesize, exact zeros
     outside the band (bandreduce.py:91-120).  Returns the padded band as a
-    column-major (Fortran-order) numpy array in the storage dtype, or a
-    device tensor holding it column-major for device input."""
+    column-major (Fortran-order) numpy array in the storage dtype, or (device
+    input) a device tensor whose value is the band, stored column-major."""
     torch = _torch()
     be = _backend(backend)
     L = _lib.lib()
@@ -221,7 +221,7 @@ def banddiag(a, cfg: KernelConfig | None = None, backend=None):
                                    ctypes.byref(opt), ws.data_ptr(), ws.numel(), be.stream_handle()))
     if host:
         return work.cpu().numpy().T          # Fortran-order view: band of A
-    return work
+    return work.t()                          # the band itself (column-major strides)
 
 
 def band_to_bidiagonal(band, bandwidth: int, backend=None):

@@ -122,6 +122,74 @@ __device__ __forceinline__ void negcount2(const double *__restrict__ o2, int64_t
     c1 = n1;
 }
 
+// K interleaved Sturm counts (identical arithmetic to negcount per chain).
+template <int K>
+__device__ __forceinline__ void negcountK(const double *__restrict__ o2, int64_t m, const double (&x)[K],
+                                          double pivmin, int (&c)[K]) {
+    double q[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        q[i] = -x[i];
+        if (fabs(q[i]) < pivmin) q[i] = (q[i] < 0.0) ? -pivmin : pivmin;
+        c[i] = q[i] < 0.0;
+    }
+    for (int64_t j = 0; j < m; ++j) {
+        const double o = __ldg(o2 + j);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            q[i] = -x[i] - sdiv(o, q[i]);
+            if (fabs(q[i]) < pivmin) q[i] = (q[i] < 0.0) ? -pivmin : pivmin;
+            c[i] += q[i] < 0.0;
+        }
+    }
+}
+
+// Multisection of the bracket N(lo) < rank <= N(hi) with K points per pass
+// (K interleaved chains in one thread: when values are scarce the stage is
+// latency-bound and K chains cost about one pass of one chain): lo moves to
+// the highest point with N < rank, hi to the next point, so the result is the
+// pair of adjacent doubles plain bisection converges to.  Stops when no
+// double lies strictly inside, hi <= floor_, or (isolate) the bracket holds
+// one value.
+template <int K>
+__device__ __forceinline__ void multisect(const double *__restrict__ ob, int64_t n, int64_t rank, double &lo,
+                                          double &hi, int64_t &clo, int64_t &chi, double pivmin, double floor_,
+                                          bool isolate) {
+    const int64_t m = 2 * n - 1;
+    for (int pass = 0; pass < 200; ++pass) {
+        if (hi <= floor_ || (isolate && chi - clo == 1)) break;
+        const double w = hi - lo;
+        double x[K];
+        bool ok[K];
+        double prev = lo;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            double t = lo + w * ((double)(i + 1) / (double)(K + 1));
+            ok[i] = t > prev && t < hi;
+            if (ok[i]) prev = t;
+            x[i] = ok[i] ? t : prev;
+        }
+        if (!ok[0] && !(0.5 * (lo + hi) > lo && 0.5 * (lo + hi) < hi)) break;   // adjacent
+        if (!ok[0]) {                       // too narrow for K points: the midpoint alone
+#pragma unroll
+            for (int i = 0; i < K; ++i) { x[i] = 0.5 * (lo + hi); ok[i] = i == 0; }
+        }
+        int c[K];
+        negcountK<K>(ob, m, x, pivmin, c);
+        double nlo = lo, nhi = hi;
+        int64_t nclo = clo, nchi = chi;
+        int top = -1;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (ok[i] && c[i] - n < rank) top = i;
+        if (top >= 0) { nlo = x[top]; nclo = c[top] - n; }
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i)
+            if (ok[i] && i > top && c[i] - n >= rank) { nhi = x[i]; nchi = c[i] - n; }
+        lo = nlo; hi = nhi; clo = nclo; chi = nchi;
+    }
+}
+
 // Sturm count (identical arithmetic to negcount) plus the Laguerre sums at x:
 // G = sum 1/(x - lambda) = (log|f|)', S2 = (log|f|)'' = -sum 1/(x - lambda)^2
 // for f(x) = det(TGK - x I), from the derivative recurrences of
@@ -165,6 +233,7 @@ __device__ __forceinline__ int sturm_laguerre(const double *__restrict__ o2, int
 // bracket invariant, so a bad step only costs a bisection.  Then two probes
 // a few ulps either side of the converged iterate and a short bisection to
 // adjacent doubles give exactly the value plain bisection would return.
+template <int K = 1>
 __device__ __forceinline__ double finish_value(const double *__restrict__ ob, int64_t n, int64_t rank,
                                                double lo, double hi, int64_t clo, int64_t chi,
                                                double pivmin, double floor_) {
@@ -212,11 +281,15 @@ __device__ __forceinline__ double finish_value(const double *__restrict__ ob, in
             }
         }
     }
-    for (int it = 0; it < 200; ++it) {               // bisection to adjacent doubles
-        const double mid = 0.5 * (lo + hi);
-        if (!(mid > lo && mid < hi) || hi <= floor_) break;
-        const int64_t cnt = negcount(ob, m, mid, pivmin) - n;
-        if (cnt < rank) lo = mid; else hi = mid;
+    if constexpr (K > 1) {                           // multisection to adjacent doubles
+        multisect<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_, false);
+    } else {
+        for (int it = 0; it < 200; ++it) {           // bisection to adjacent doubles
+            const double mid = 0.5 * (lo + hi);
+            if (!(mid > lo && mid < hi) || hi <= floor_) break;
+            const int64_t cnt = negcount(ob, m, mid, pivmin) - n;
+            if (cnt < rank) lo = mid; else hi = mid;
+        }
     }
     return lo;
 }
@@ -330,7 +403,7 @@ __global__ void __launch_bounds__(128) k_slice(const double *__restrict__ o2,
 // One thread per value: its cell from the slice counts (binary search for
 // the first x_p with N(x_p) >= rank), bisection until the value is isolated,
 // then finish_value (Laguerre + probes + bisection to adjacent doubles).
-template <typename OutT>
+template <typename OutT, int K>
 __global__ void __launch_bounds__(128) k_values(const double *__restrict__ o2,
                                                 const double *__restrict__ scal,
                                                 const int *__restrict__ cnt, int P, int64_t n,
@@ -358,14 +431,18 @@ __global__ void __launch_bounds__(128) k_values(const double *__restrict__ o2,
         if (!(clo < rank && rank <= chi)) {              // non-monotone counts: full range
             lo = 0.0; hi = 2.0 * gersh; clo = 0; chi = n;
         }
-        for (int it = 0; it < 64; ++it) {                // bisect until isolated
-            if (hi <= floor_ || chi - clo == 1) break;
-            const double mid = 0.5 * (lo + hi);
-            if (!(mid > lo && mid < hi)) break;
-            const int64_t c = negcount(ob, 2 * n - 1, mid, pivmin) - n;
-            if (c < rank) { lo = mid; clo = c; } else { hi = mid; chi = c; }
+        if constexpr (K > 1) {
+            multisect<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_, true);   // until isolated
+        } else {
+            for (int it = 0; it < 64; ++it) {            // bisect until isolated
+                if (hi <= floor_ || chi - clo == 1) break;
+                const double mid = 0.5 * (lo + hi);
+                if (!(mid > lo && mid < hi)) break;
+                const int64_t c = negcount(ob, 2 * n - 1, mid, pivmin) - n;
+                if (c < rank) { lo = mid; clo = c; } else { hi = mid; chi = c; }
+            }
         }
-        res = finish_value(ob, n, rank, lo, hi, clo, chi, pivmin, floor_) * unscale;
+        res = finish_value<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_) * unscale;
     }
     out[b * out_stride + k] = (OutT)res;
 }
@@ -404,8 +481,18 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
         // (one warp per block while that leaves SMs idle; batches fill them anyway)
         const int vb = getenv("BSVD_VALUES_BLOCK") ? atoi(getenv("BSVD_VALUES_BLOCK"))
                        : (n_out * batch >= 148 * 128 ? 128 : 32);
-        k_values<OutT><<<dim3((unsigned)((n_out + vb - 1) / vb), (unsigned)batch), vb, 0, st>>>(
-            o2, scal, cnt, P, n, n_out, out, out_stride);
+        // BSVD_VALUES_K=4/8: multisection with K interleaved chains per thread
+        // (same values bit for bit; measured at 8192: K=4 21.0 ms, K=8 69.7 ms
+        // against 20.8 ms for bisection -- the chains do not come for free)
+        int K = 1;
+        if (const char *e = getenv("BSVD_VALUES_K")) K = atoi(e) == 8 ? 8 : (atoi(e) == 4 ? 4 : 1);
+        const dim3 vg((unsigned)((n_out + vb - 1) / vb), (unsigned)batch);
+        if (K == 8)
+            k_values<OutT, 8><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
+        else if (K == 4)
+            k_values<OutT, 4><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
+        else
+            k_values<OutT, 1><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
         bsvd_host::count_launch();
         return cudaGetLastError();
     }

@@ -299,8 +299,13 @@ def test_stage_entry_points_row_major_tensor(P, be_tree, oracle, dtype):
     full = rng.standard_normal((128, 128)).astype(dtype)
     band_dev = P.banddiag(torch.from_numpy(full).cuda(), P.KernelConfig(tilesize=32), backend=be_tree)
     band_host = P.banddiag(full, P.KernelConfig(tilesize=32), backend=be_tree)
-    # device result holds the band column-major (row-major storage of band^T)
-    assert np.allclose(band_dev.cpu().numpy().T, band_host, atol=1e-4 if dtype == np.float32 else 1e-12)
+    # device result: the band itself, column-major strides; feeds the chase as is
+    assert band_dev.stride(0) == 1
+    assert np.allclose(band_dev.cpu().numpy(), band_host, atol=1e-4 if dtype == np.float32 else 1e-12)
+    d2, e2 = P.band_to_bidiagonal(band_dev, 32, backend=be_tree)
+    want2 = np.linalg.svd(band_host.astype(np.float64), compute_uv=False)
+    assert_close(oracle.bidiagonal_values(d2.cpu().numpy(), e2.cpu().numpy()), want2, dtype, 128,
+                 what="banddiag -> band_to_bidiagonal on the device")
 
 
 def test_padded_dense_matrix_returns_orig_n(P, be_tree, oracle):
