@@ -94,6 +94,67 @@ def write_matrix(m: DenseMatrix, path) -> None:
         f.write(np.ascontiguousarray(m.data, dtype=le).tobytes())
 
 
+def _read_header(path):
+    """(dtype, rows, cols, payload bytes) with the reference's format errors
+    (matrix.py:230-249), reading only the 28-byte header."""
+    import os
+    size = os.path.getsize(path)
+    with open(path, "rb") as f:
+        head = f.read(28)
+    if len(head) < 4 or head[:4] != _MAGIC:
+        raise FormatError(f"bad magic {head[:4]!r}, expected {_MAGIC!r}")
+    if len(head) < 28:
+        raise FormatError("truncated header")
+    version, code, rows, cols = struct.unpack("<IIQQ", head[4:28])
+    if version != _FORMAT_VERSION:
+        raise FormatError(f"unknown format version {version}")
+    if code not in _DTYPE_CODES:
+        raise FormatError(f"unknown dtype code {code}")
+    dtype = _DTYPE_CODES[code]
+    expected = rows * cols * dtype.itemsize
+    payload = size - 28
+    if payload < expected:
+        raise FormatError(f"truncated payload: {payload} bytes, expected {expected}")
+    if payload > expected:
+        raise FormatError(f"payload has {payload - expected} trailing bytes")
+    return dtype, int(rows), int(cols)
+
+
+def read_matrix_device(path, device=None, chunk_bytes: int = 64 << 20):
+    """BSVD file -> device tensor without a host copy of the whole payload:
+    the payload is memory-mapped and streamed through two pinned staging
+    buffers (the read of chunk i+1 overlaps the H2D copy of chunk i on a side
+    stream).  Returns (tensor [rows, cols] whose memory is the column-major
+    matrix -- i.e. the transposed view of the payload, as ``svdvals`` and
+    ``banddiag`` consume it --, precision).  SURVEY.md 8(f) row 2."""
+    import torch
+    dtype, rows, cols = _read_header(path)
+    native = dtype.newbyteorder("=")
+    mm = np.memmap(path, dtype=dtype, mode="r", offset=28, shape=(rows * cols,))
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    tdt = {1: torch.float64, 2: torch.float32, 3: torch.float16}[
+        {np.dtype("<f8"): 1, np.dtype("<f4"): 2, np.dtype("<f2"): 3}[np.dtype(dtype)]]
+    out = torch.empty(rows * cols, dtype=tdt, device=dev)
+    per = max(1, chunk_bytes // dtype.itemsize)
+    bufs = [torch.empty(min(per, rows * cols), dtype=tdt, pin_memory=True) for _ in range(2)]
+    events = [None, None]
+    stream = torch.cuda.Stream(device=dev)
+    for i, lo in enumerate(range(0, rows * cols, per)):
+        hi = min(rows * cols, lo + per)
+        b = i & 1
+        if events[b] is not None:
+            events[b].synchronize()          # the copy out of this buffer is done
+        bufs[b].numpy()[: hi - lo] = mm[lo:hi].astype(native, copy=False)
+        with torch.cuda.stream(stream):
+            out[lo:hi].copy_(bufs[b][: hi - lo], non_blocking=True)
+            events[b] = torch.cuda.Event()
+            events[b].record(stream)
+    torch.cuda.current_stream(dev).wait_stream(stream)
+    out.record_stream(stream)
+    del mm
+    return out.view(cols, rows).t(), from_storage_dtype(np.dtype(native))
+
+
 def read_matrix(path) -> DenseMatrix:
     """Inverse of write_matrix with the reference's format errors (:230-249)."""
     with open(path, "rb") as f:

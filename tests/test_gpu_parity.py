@@ -395,3 +395,20 @@ def test_reference_driver_on_b200_backend(P, be_faithful, name, splitk):
     B.banddiag(work, tau, N, B.KernelConfig(tilesize=ts, splitk=splitk), be_faithful)
     assert be_faithful.stats.launches > before
     assert same_bits(np.asfortranarray(work.array), np.asfortranarray(g["band"]))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.float16])
+def test_read_matrix_device_streams_the_file(P, be_tree, tmp_path, dtype):
+    """BSVD file -> mmap -> pinned chunks -> device: the
+    device tensor is the file's matrix, and svdvals on it equals svdvals on
+    the host-read DenseMatrix bit for bit."""
+    from paper_2508_06339_b200.matrix import DenseMatrix, read_matrix, read_matrix_device, write_matrix
+    a = np.random.default_rng(21).standard_normal((300, 300)).astype(dtype)
+    path = str(tmp_path / "m.bsvd")
+    write_matrix(DenseMatrix.from_array(a), path)
+    t, prec = read_matrix_device(path, be_tree.device, chunk_bytes=4096)   # many chunks
+    assert t.shape == (300, 300) and t.stride(0) == 1
+    assert np.array_equal(t.cpu().numpy(), a)
+    got = P.svdvals(t, P.KernelConfig(tilesize=64), backend=be_tree).cpu().numpy()
+    want = P.svdvals(read_matrix(path), P.KernelConfig(tilesize=64), backend=be_tree)
+    assert np.array_equal(got, want)
