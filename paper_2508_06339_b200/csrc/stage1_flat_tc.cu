@@ -208,11 +208,18 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
                 const uint32_t bh = gtile ? ah : tc::smem_u32(base + 2 * IMG);
                 const uint32_t bl = gtile ? al : tc::smem_u32(base + 3 * IMG);
                 const uint32_t acc = tmem + (uint32_t)(ab * BN);
+                // the small cross terms first, the hi*hi products last: the
+                // accumulator only reaches full magnitude for the last K/8 adds
+                // (each TMEM accumulation rounds relative to the accumulator)
 #pragma unroll
                 for (int k = 0; k < KB / 8; ++k) {
                     const uint32_t o = 32u * k;
                     tc::mma_tf32(acc, tc::sdesc(ah + o), tc::sdesc(bl + o), id, !first || k > 0);
                     tc::mma_tf32(acc, tc::sdesc(al + o), tc::sdesc(bh + o), id, true);
+                }
+#pragma unroll
+                for (int k = 0; k < KB / 8; ++k) {
+                    const uint32_t o = 32u * k;
                     tc::mma_tf32(acc, tc::sdesc(ah + o), tc::sdesc(bh + o), id, true);
                 }
                 tc::commit(&empty[st]);
