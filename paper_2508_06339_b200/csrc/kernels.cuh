@@ -52,14 +52,15 @@ cudaError_t banddiag_flat(S *a, int64_t n, int ts, int64_t batch, int64_t a_bstr
                           cudaStream_t st, double *panel_ms, double *trail_ms);
 
 // ---- stage1_flat_tc.cu (tcgen05 3xTF32 trailing-update products, TMA-fed;
-// ts = 128, FP32 storage)
+// ts = 128, FP32 / FP16 storage)
 bool flat_tc_supported(int ts, int elem_bytes);
 struct FlatTcPlan;
-FlatTcPlan *flat_tc_plan(float *a, int64_t n, int64_t batch, int64_t a_bstride, const float *vcm0, const float *vcm1,
-                         const float *vrm0, const float *vrm1, const float *w2t, int64_t ws_bstride);
+FlatTcPlan *flat_tc_plan(void *a, int elem_bytes, int64_t n, int64_t batch, int64_t a_bstride, const float *vcm0,
+                         const float *vcm1, const float *vrm0, const float *vrm1, const float *w2t,
+                         int64_t ws_bstride);
 void flat_tc_plan_free(FlatTcPlan *p);
 cudaError_t launch_flat_tc(const FlatTcPlan *plan, int par, int mode, bool lq, int M, int C, int row_base,
-                           int col_base, float *Wp, float *Gp, int64_t ws_bstride, int ns, int rps, float *a,
+                           int col_base, float *Wp, float *Gp, int64_t ws_bstride, int ns, int rps, void *a,
                            int64_t n, int64_t a_bstride, int64_t batch, cudaStream_t st);
 
 // ---- stage1_apply.cu (per-level WY trailing updates, ts >= 16) ----------

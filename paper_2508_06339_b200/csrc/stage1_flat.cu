@@ -1721,8 +1721,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         if constexpr (TS == 128)
             if ((e = ensure_smem(k_tbuild<TS>, tbuild_smem)) != cudaSuccess) return e;
         const Ws w0 = ws_carve(ws, n, TS, nsplit);
-        tcp = flat_tc_plan(reinterpret_cast<float *>(a), n, batch, a_bstride, w0.Vcm0, w0.Vcm1, w0.Vrm0, w0.Vrm1,
-                           w0.W2T, wsb);
+        tcp = flat_tc_plan(a, (int)sizeof(S), n, batch, a_bstride, w0.Vcm0, w0.Vcm1, w0.Vrm0, w0.Vrm1, w0.W2T, wsb);
         if (!tcp) return cudaErrorNotSupported;
     }
     // development knob: BSVD_FLAT_TC=2 -> only the W product on the tensor
@@ -1795,7 +1794,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
             if (tc1)
             {
                 e2 = launch_flat_tc(tcp, par, 1, lq, M, C, (int)(top * TS), (int)((k + 1) * TS), w0.Wp, w0.Gp, wsb, ns,
-                                    rps, reinterpret_cast<float *>(a), n, a_bstride, batch, su);
+                                    rps, a, n, a_bstride, batch, su);
                 if (e2 == cudaSuccess) {
                     if constexpr (TS == 128) {
                         k_tbuild<TS><<<(unsigned)batch, kTB, tbuild_smem, su>>>(ws, wsb, n, nsplit, ns);
@@ -1832,7 +1831,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
                 const dim3 g2((unsigned)((M - TS + 127) / 128), (unsigned)cblk, (unsigned)batch);
                 if (tc2) {
                     e2 = launch_flat_tc(tcp, par, 2, lq, M, C, (int)(top * TS), (int)((k + 1) * TS), w0.Wp, w0.Gp, wsb,
-                                        1, 0, reinterpret_cast<float *>(a), n, a_bstride, batch, su);
+                                        1, 0, a, n, a_bstride, batch, su);
                     if (e2 != cudaSuccess) return e2;
                 } else if (lq)
                     k_fgemm2<S, TS, false><<<g2, kGT, 0, su>>>(X, rs, a_bstride, M, C, ws, wsb, n, nsplit, par);

@@ -27,10 +27,17 @@
 //   G1:                       D[j][c] = sum_r Vcm[j][r] X(r, c)
 // All operands are K-major in memory except X in G1 on the LQ side, whose raw
 // [32 r][128 c] box is transposed by the split warps.
+//
+// FP16 storage (H): X is exactly representable in tf32 (11 significant bits),
+// so its lo part is zero: X's boxes land raw (fp16, unswizzled) in the B_lo
+// slot, the split warps widen them into the fp32 B_hi image, and the
+// A_hi * B_lo product is skipped (two MMAs per K = 8 step instead of three);
+// the X update reads and writes fp16 (round to nearest).
 #include <cuda.h>
 #include <stdio.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -76,7 +83,7 @@ struct Args {
     float *Wp;              // G1 output (member 0)
     float *Gp;              // G1's Gram partials [ns][TS][TS] (member 0)
     int64_t ws_bstride;     // floats
-    float *X;               // G2 epilogue: matrix base (member 0)
+    void *X;                // G2 epilogue: matrix base (member 0), storage type
     int64_t n, a_bstride;   // G2 epilogue: leading dim, batch stride
 };
 
@@ -112,7 +119,7 @@ __device__ __forceinline__ void split_image(float *hi, float *lo, int t) {
     }
 }
 
-template <int MODE, bool LQ>
+template <int MODE, bool LQ, bool H>
 __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps maps, const Args g) {
     using CF = Cfg<MODE>;
     constexpr int NST = CF::NST;
@@ -166,20 +173,22 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
                 // RQ: inner = rows (m), outer = cols (n); LQ: inner = cols (m), outer = rows (n)
                 const int inner = (LQ ? g.col_base : g.row_base) + m0;
                 const int outer = (LQ ? g.row_base : g.col_base) + n0;
-                expect_tx(&xload, (uint32_t)(BM * BN * 4));
+                expect_tx(&xload, (uint32_t)(BM * BN * (H ? 2 : 4)));
                 tma3(xt, &maps.Xt, &xload, inner, outer, b);
             }
             for (int kb = 0; kb < nkb; ++kb) {
                 const int st = kb % NST;
                 if (kb >= NST) tc::mbar_wait(&empty[st], (uint32_t)((kb / NST - 1) & 1));
                 float *base = sm + st * STAGE;
-                expect_tx(&loaded[st], (uint32_t)((gtile ? 1 : 2) * IMG * 4));
+                const uint32_t bbytes = MODE == 1 && H ? IMG * 2 : IMG * 4;   // fp16 X box: half the bytes
+                expect_tx(&loaded[st], (uint32_t)(IMG * 4 + (gtile ? 0 : bbytes)));
                 const int kk = kb * KB;
                 if (MODE == 1) {
                     tma3(base, &maps.Vcm, &loaded[st], k_lo + kk, 0, b);              // A[j][r]
                     if (gtile) {
                     } else if (!LQ)   // B[c][r]: X(r, c) at inner = row_base + r, outer = col_base + c
-                        tma3(base + 2 * IMG, &maps.Xk, &loaded[st], g.row_base + k_lo + kk, g.col_base + n0, b);
+                        tma3(base + (H ? 3 : 2) * IMG, &maps.Xk, &loaded[st], g.row_base + k_lo + kk,
+                             g.col_base + n0, b);
                     else       // raw [32 r][128 c]: inner = col_base + c, outer = row_base + r
                         tma3(base + 3 * IMG, &maps.Xm, &loaded[st], g.col_base + n0, g.row_base + k_lo + kk, b);
                 } else if (!LQ) {
@@ -211,11 +220,12 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
                 // the small cross terms first, the hi*hi products last: the
                 // accumulator only reaches full magnitude for the last K/8 adds
                 // (each TMEM accumulation rounds relative to the accumulator)
+                const bool b_exact = MODE == 1 && H && !gtile;   // fp16 X: lo == 0
 #pragma unroll
                 for (int k = 0; k < KB / 8; ++k) {
                     const uint32_t o = 32u * k;
-                    tc::mma_tf32(acc, tc::sdesc(ah + o), tc::sdesc(bl + o), id, !first || k > 0);
-                    tc::mma_tf32(acc, tc::sdesc(al + o), tc::sdesc(bh + o), id, true);
+                    if (!b_exact) tc::mma_tf32(acc, tc::sdesc(ah + o), tc::sdesc(bl + o), id, !first || k > 0);
+                    tc::mma_tf32(acc, tc::sdesc(al + o), tc::sdesc(bh + o), id, !b_exact || !first || k > 0);
                 }
 #pragma unroll
                 for (int k = 0; k < KB / 8; ++k) {
@@ -257,6 +267,32 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
             float *base = sm + st * STAGE;
             split_image(base, base + IMG, t);                 // A in place
             if (gtile) {
+            } else if (MODE == 1 && H) {
+                // raw fp16 box in the B_lo slot -> fp32 B_hi image (exact)
+                const __half *raw = reinterpret_cast<const __half *>(base + 3 * IMG);
+                float4 v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int ch = t + i * NSW * 32;
+                    if (!LQ) {      // raw [128 c][32 r]: 4 consecutive r of one c
+                        const int c = ch >> 3, r4 = (ch & 7) * 4;
+                        const uint2 u = *reinterpret_cast<const uint2 *>(raw + c * KB + r4);
+                        const float2 x0 = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+                        const float2 x1 = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+                        v[i] = make_float4(x0.x, x0.y, x1.x, x1.y);
+                    } else {        // raw [32 r][128 c]: lanes over c
+                        const int c = ch & (BN - 1), r4 = (ch >> 7) * 4;
+                        const __half *rp = raw + r4 * BN + c;
+                        v[i] = make_float4(__half2float(rp[0]), __half2float(rp[BN]), __half2float(rp[2 * BN]),
+                                           __half2float(rp[3 * BN]));
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int ch = t + i * NSW * 32;
+                    const int c = LQ ? (ch & (BN - 1)) : ch >> 3, r4 = LQ ? (ch >> 7) * 4 : (ch & 7) * 4;
+                    *reinterpret_cast<float4 *>(base + 2 * IMG + tc::img_off(c, r4, 0)) = v[i];
+                }
             } else if (MODE == 1 && LQ) {
                 // raw [32 r][128 c] in the B_lo slot -> K-major images [c][r]:
                 // thread chunk = (c, 4 consecutive r); lanes run over c, so the
@@ -292,7 +328,9 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
         // ---------------- epilogue (sum = the accumulated tile row m) ----------
         if (MODE == 2) tc::mbar_wait(&xload, 0);
         const int64_t wo = (int64_t)b * g.ws_bstride;
-        float *X = g.X + (int64_t)b * g.a_bstride;
+        using ST = typename std::conditional<H, __half, float>::type;
+        ST *X = reinterpret_cast<ST *>(g.X) + (int64_t)b * g.a_bstride;
+        const ST *xts = reinterpret_cast<const ST *>(xt);
         // G2 destination: X(lane m, column c) at X[(outer0 + c) * n + inner0 + m]
         const int64_t inner0 = (LQ ? g.col_base : g.row_base) + m0, outer0 = (LQ ? g.row_base : g.col_base) + n0;
         const int c0 = chalf * 64;
@@ -304,8 +342,15 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
                 *reinterpret_cast<float4 *>(dst + i) = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
         } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
-                X[(outer0 + c0 + i) * g.n + inner0 + m] = xt[(c0 + i) * BM + m] - sum[i];
+            for (int i = 0; i < 64; ++i) {
+                const float x = H ? __half2float(reinterpret_cast<const __half *>(xts)[(c0 + i) * BM + m])
+                                  : reinterpret_cast<const float *>(xts)[(c0 + i) * BM + m];
+                const float y = x - sum[i];
+                if constexpr (H)
+                    X[(outer0 + c0 + i) * g.n + inner0 + m] = __float2half_rn(y);
+                else
+                    X[(outer0 + c0 + i) * g.n + inner0 + m] = y;
+            }
         }
     }
     tc::fence_before();
@@ -331,16 +376,19 @@ static EncodeFn encode_fn() {
     });
     return fn;
 }
-// 3-D fp32 map: dims {inner, outer, batch}, strides in bytes of outer / batch
-static bool make_map(CUtensorMap *m, const float *base, uint64_t inner, uint64_t outer, uint64_t batch,
-                     uint64_t outer_stride, uint64_t batch_stride, uint32_t box_in, uint32_t box_out, bool sw128) {
+// 3-D map: dims {inner, outer, batch}, element strides of outer / batch;
+// esz 4 (fp32) or 2 (fp16)
+static bool make_map(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer, uint64_t batch,
+                     uint64_t outer_stride, uint64_t batch_stride, uint32_t box_in, uint32_t box_out, bool sw128,
+                     int esz = 4) {
     EncodeFn fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[3] = {inner, outer, batch};
-    const cuuint64_t strides[2] = {outer_stride * 4, (batch > 1 ? batch_stride : outer_stride * outer) * 4};
+    const cuuint64_t strides[2] = {outer_stride * esz, (batch > 1 ? batch_stride : outer_stride * outer) * esz};
     const cuuint32_t box[3] = {box_in, box_out, 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, es,
+    return fn(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+              const_cast<void *>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -350,22 +398,27 @@ static bool make_map(CUtensorMap *m, const float *base, uint64_t inner, uint64_t
 bool flat_tc_supported(int ts, int elem_bytes) {
     if (const char *s = getenv("BSVD_FLAT_TC"))
         if (atoi(s) == 0) return false;
-    return ts == 128 && elem_bytes == 4 && ftc::encode_fn() != nullptr;
+    return ts == 128 && (elem_bytes == 4 || elem_bytes == 2) && ftc::encode_fn() != nullptr;
 }
 
 struct FlatTcPlan {
     ftc::Maps maps[2];   // by V ping-pong parity
+    bool half;           // FP16 storage
 };
 
-FlatTcPlan *flat_tc_plan(float *a, int64_t n, int64_t batch, int64_t a_bstride, const float *vcm0, const float *vcm1,
-                         const float *vrm0, const float *vrm1, const float *w2t, int64_t ws_bstride) {
+FlatTcPlan *flat_tc_plan(void *a, int elem_bytes, int64_t n, int64_t batch, int64_t a_bstride, const float *vcm0,
+                         const float *vcm1, const float *vrm0, const float *vrm1, const float *w2t,
+                         int64_t ws_bstride) {
     auto *p = new FlatTcPlan;
+    p->half = elem_bytes == 2;
+    const int es = p->half ? 2 : 4;
     bool ok = true;
     for (int par = 0; par < 2; ++par) {
         ftc::Maps &m = p->maps[par];
-        ok = ok && ftc::make_map(&m.Xk, a, n, n, batch, n, a_bstride, 32, 128, true);
-        ok = ok && ftc::make_map(&m.Xm, a, n, n, batch, n, a_bstride, 128, 32, false);
-        ok = ok && ftc::make_map(&m.Xt, a, n, n, batch, n, a_bstride, 128, 128, false);
+        // fp16 X: raw unswizzled boxes (widened by the split warps)
+        ok = ok && ftc::make_map(&m.Xk, a, n, n, batch, n, a_bstride, 32, 128, !p->half, es);
+        ok = ok && ftc::make_map(&m.Xm, a, n, n, batch, n, a_bstride, 128, 32, false, es);
+        ok = ok && ftc::make_map(&m.Xt, a, n, n, batch, n, a_bstride, 128, 128, false, es);
         ok = ok && ftc::make_map(&m.Vcm, par ? vcm1 : vcm0, n, 128, batch, n, ws_bstride, 32, 128, true);
         ok = ok && ftc::make_map(&m.Vrm, par ? vrm1 : vrm0, 128, n, batch, 128, ws_bstride, 32, 128, true);
         ok = ok && ftc::make_map(&m.W2T, w2t, 128, n, batch, 128, ws_bstride, 32, 128, true);
@@ -379,7 +432,7 @@ FlatTcPlan *flat_tc_plan(float *a, int64_t n, int64_t batch, int64_t a_bstride, 
 void flat_tc_plan_free(FlatTcPlan *p) { delete p; }
 
 cudaError_t launch_flat_tc(const FlatTcPlan *plan, int par, int mode, bool lq, int M, int C, int row_base,
-                           int col_base, float *Wp, float *Gp, int64_t ws_bstride, int ns, int rps, float *a,
+                           int col_base, float *Wp, float *Gp, int64_t ws_bstride, int ns, int rps, void *a,
                            int64_t n, int64_t a_bstride, int64_t batch, cudaStream_t st) {
     using namespace ftc;
     Args g{M, C, row_base, col_base, rps, Wp, Gp, ws_bstride, a, n, a_bstride};
@@ -388,12 +441,14 @@ cudaError_t launch_flat_tc(const FlatTcPlan *plan, int par, int mode, bool lq, i
     cudaError_t e;
     if (mode == 1) {
         grid = dim3((unsigned)(C / BN + 1), (unsigned)ns, (unsigned)batch);   // + the Gram tile
-        auto kern = lq ? k_tgemm<1, true> : k_tgemm<1, false>;
+        auto kern = plan->half ? (lq ? k_tgemm<1, true, true> : k_tgemm<1, false, true>)
+                               : (lq ? k_tgemm<1, true, false> : k_tgemm<1, false, false>);
         if ((e = ensure_smem(kern, Cfg<1>::SMEM)) != cudaSuccess) return e;
         kern<<<grid, NTH, Cfg<1>::SMEM, st>>>(maps, g);
     } else {
         grid = dim3((unsigned)((M - TS) / BM), (unsigned)(C / BN), (unsigned)batch);
-        auto kern = lq ? k_tgemm<2, true> : k_tgemm<2, false>;
+        auto kern = plan->half ? (lq ? k_tgemm<2, true, true> : k_tgemm<2, false, true>)
+                               : (lq ? k_tgemm<2, true, false> : k_tgemm<2, false, false>);
         if ((e = ensure_smem(kern, Cfg<2>::SMEM)) != cudaSuccess) return e;
         kern<<<grid, NTH, Cfg<2>::SMEM, st>>>(maps, g);
     }
