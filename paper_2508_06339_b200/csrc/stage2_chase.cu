@@ -966,10 +966,34 @@ __device__ __forceinline__ void left_t(Tile<T, BK, NW> &x, const T *p, int L, T 
             for (int a = 1; a < RA; ++a) t = fma(va[a], x.v[a][q], t);
             part[q] = t;
         }
+        if constexpr (CQ == 8) {
+            // reduce-scatter (lane bits 4,3,2 pick q; bits 1,0 finish the sum)
+            // then broadcast: 17 shuffles instead of a 40-shuffle butterfly
+            const unsigned F = 0xffffffffu;
+            const bool hb = l & 16, mb = l & 8, lb = l & 4;
+            T e1[4], e2[2];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+            for (int t = 0; t < 4; ++t) {
+                const T mine = hb ? part[4 + t] : part[t], oth = hb ? part[t] : part[4 + t];
+                e1[t] = mine + __shfl_xor_sync(F, oth, 16);
+            }
 #pragma unroll
-            for (int q = 0; q < CQ; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+            for (int t = 0; t < 2; ++t) {
+                const T mine = mb ? e1[2 + t] : e1[t], oth = mb ? e1[t] : e1[2 + t];
+                e2[t] = mine + __shfl_xor_sync(F, oth, 8);
+            }
+            T e3 = (lb ? e2[1] : e2[0]) + __shfl_xor_sync(F, lb ? e2[0] : e2[1], 4);
+            e3 += __shfl_xor_sync(F, e3, 2);
+            e3 += __shfl_xor_sync(F, e3, 1);
+            // lane with bits (h, m, l) holds q = 4h + 2m + l
+#pragma unroll
+            for (int q = 0; q < 8; ++q) part[q] = __shfl_sync(F, e3, ((q >> 2) << 4) | (((q >> 1) & 1) << 3) | ((q & 1) << 2));
+        } else {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int q = 0; q < CQ; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+        }
 #pragma unroll
         for (int q = 0; q < CQ; ++q) {
             const T tw = tau * part[q];
@@ -1022,13 +1046,63 @@ __device__ __forceinline__ void right_t(Tile<T, BK, NW> &x, const T *p, int L, T
     }
 }
 
+// right_t on the new block (x0) and the carried block (x1, carrier) with one
+// shared-memory reduction round (red[2][NW][BK]) for both.
+template <typename T, int BK, int NW>
+__device__ __forceinline__ void right_t2(Tile<T, BK, NW> &x0, Tile<T, BK, NW> &x1, const T *p, int L, T tau,
+                                         T scale, T beta, T *red) {
+    constexpr int RA = Tile<T, BK, NW>::RA, CQ = Tile<T, BK, NW>::CQ;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (tau != T(0)) {                     // uniform across the CTA
+        T vq[CQ];
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) {
+            const int c = w + NW * q;
+            vq[q] = c == 0 ? T(1) : (c < L ? p[c] * scale : T(0));
+        }
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            T t0 = x0.v[a][0] * vq[0], t1 = x1.v[a][0] * vq[0];
+#pragma unroll
+            for (int q = 1; q < CQ; ++q) {
+                t0 = fma(x0.v[a][q], vq[q], t0);
+                t1 = fma(x1.v[a][q], vq[q], t1);
+            }
+            red[w * BK + l + 32 * a] = t0;
+            red[(NW + w) * BK + l + 32 * a] = t1;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            const int r = l + 32 * a;
+            T d0 = T(0), d1 = T(0);
+#pragma unroll
+            for (int g = 0; g < NW; ++g) {
+                d0 += red[g * BK + r];
+                d1 += red[(NW + g) * BK + r];
+            }
+            const T td0 = tau * d0, td1 = tau * d1;
+#pragma unroll
+            for (int q = 0; q < CQ; ++q) {
+                x0.v[a][q] = fma(-td0, vq[q], x0.v[a][q]);
+                x1.v[a][q] = fma(-td1, vq[q], x1.v[a][q]);
+            }
+        }
+        __syncthreads();                   // red is reused by the next right op
+    }
+    if (l == 0) {
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) x1.v[0][q] = (w + NW * q == 0) ? beta : T(0);
+    }
+}
+
 template <typename T, int BK, int NW>
 __global__ void __launch_bounds__(NW * 32) k_chase_cta(T *band, int64_t n, int b, int64_t ld,
                                                       int64_t batch) {
     using TL = Tile<T, BK, NW>;
     constexpr int RA = TL::RA, CQ = TL::CQ;
     __shared__ T piv[BK];
-    __shared__ T red[NW * BK];
+    __shared__ T red[2 * NW * BK];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int64_t m = blockIdx.x; m < batch; m += gridDim.x) {
         const ch2::BandT<T> A{band + m * n * ld, n, ld, b};
@@ -1050,9 +1124,10 @@ __global__ void __launch_bounds__(NW * 32) k_chase_cta(T *band, int64_t n, int b
                 if (k & 1) {
                     left_t<T, BK, NW>(xn, piv, L, tau, scale, beta, false);
                     left_t<T, BK, NW>(xc, piv, L, tau, scale, beta, true);
+                } else if (k > 0) {
+                    right_t2<T, BK, NW>(xn, xc, piv, L, tau, scale, beta, red);
                 } else {
                     right_t<T, BK, NW>(xn, piv, L, tau, scale, beta, false, red);
-                    if (k > 0) right_t<T, BK, NW>(xc, piv, L, tau, scale, beta, true, red);
                 }
                 if (k > 0) store_t<T, BK, NW>(A, gc, xc);               // block k-1 is final
                 __syncthreads();                                        // piv fully consumed
@@ -1224,6 +1299,7 @@ cudaError_t band_to_bidiagonal(const S *a, int64_t n, int64_t lda, int bw, int64
             bsvd_host::count_launch();
             auto kern = ch3::k_chase_cta<float, 64, 8>;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+            if (const char *e = getenv("BSVD_CTA_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
             kern<<<(unsigned)std::min<int64_t>(batch, (int64_t)nsm * std::max(per_sm, 1)), 256, 0, st>>>(
                 (float *)bandp, n, b, ld, batch);
             bsvd_host::count_launch();
