@@ -63,7 +63,7 @@ bool use_flat(bsvd_dtype dt, int ts) { return flat_supported(ts, dt == BSVD_FP64
 struct Plan {
     int64_t n, N, np, batch;
     int ts;
-    size_t off_flag, off_work, off_d, off_e, off_scratch, total;
+    size_t off_flag, off_scale, off_work, off_d, off_e, off_scratch, total;
     size_t stage1_bytes, chase_bytes, bisect_bytes;
 };
 
@@ -92,6 +92,7 @@ Plan make_plan(bsvd_dtype dt, int64_t n, int64_t batch, const bsvd_config &c, in
     p.bisect_bytes = align_up(bisect_workspace_bytes(p.np, batch));
     size_t off = 0;
     p.off_flag = off;  off += 256;
+    p.off_scale = off; off += align_up((size_t)batch * 16);   // amax bits | unscale
     p.off_work = off;  off += align_up((size_t)batch * p.np * p.np * es);
     p.off_d = off;     off += align_up((size_t)batch * p.np * 8);
     p.off_e = off;     off += align_up((size_t)batch * p.np * 8);
@@ -163,7 +164,12 @@ bsvd_status pipeline(const S *a, const Plan &p, int64_t lda, int64_t stride,
     double *e = (double *)(ws + p.off_e);
     char *scratch = ws + p.off_scratch;
     BSVD_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    cudaError_t err = copy_in_pad<S>(a, p.n, lda, stride, work, p.np, p.batch, flag, st);
+    // fast path: power-of-two normalisation (util.cu); the faithful path keeps
+    // the reference's scale-dependent arithmetic
+    const bool norm = opt.stage1_algo != BSVD_STAGE1_FAITHFUL;
+    unsigned long long *amax = norm ? (unsigned long long *)(ws + p.off_scale) : nullptr;
+    double *unscale = norm ? (double *)(ws + p.off_scale) + p.batch : nullptr;
+    cudaError_t err = copy_in_pad<S>(a, p.n, lda, stride, work, p.np, p.batch, flag, st, amax, unscale);
     if (err != cudaSuccess) return cuda_error(err, "copy-in");
     if (opt.check_finite) {
         int h = 0;
@@ -185,6 +191,8 @@ bsvd_status pipeline(const S *a, const Plan &p, int64_t lda, int64_t stride,
     if (timers) cudaEventRecord(e1, st);
     err = bidiagonal_values<C>(d, e, p.np, p.batch, values, p.n, p.n, scratch, st);
     if (err != cudaSuccess) return cuda_error(err, "stage 3 (bisection)");
+    if (norm && (err = unscale_values<C>(values, p.n, p.n, p.batch, unscale, st)) != cudaSuccess)
+        return cuda_error(err, "unscale");
     if (timers) {
         cudaEventRecord(e2, st);
         cudaEventSynchronize(e2);

@@ -100,9 +100,12 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
 size_t bisect_workspace_bytes(int64_t n, int64_t batch);
 
 // ---- util.cu ---------------------------------------------------------------
+template <typename C>
+cudaError_t unscale_values(C *v, int64_t n, int64_t stride, int64_t batch, const double *unscale, cudaStream_t st);
 template <typename S>
 cudaError_t copy_in_pad(const S *src, int64_t n, int64_t lda, int64_t src_bstride, S *dst,
-                        int64_t np, int64_t batch, int *nonfinite_flag, cudaStream_t st);
+                        int64_t np, int64_t batch, int *nonfinite_flag, cudaStream_t st,
+                        unsigned long long *amax = nullptr, double *unscale = nullptr);
 template <typename S>
 cudaError_t clear_outside_band(S *a, int64_t n, int bw, int64_t batch, cudaStream_t st);
 

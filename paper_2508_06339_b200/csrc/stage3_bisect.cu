@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(128) k_values(const double *__restrict__ o2,
 }
 
 static int slice_points(int64_t n) {
-    int64_t P = 4 * n;
+    static const int per = getenv("BSVD_SLICE_PER") ? atoi(getenv("BSVD_SLICE_PER")) : 4;
+    int64_t P = per * n;
     if (P < 256) P = 256;
     if (P > 65536) P = 65536;
     return (int)P;

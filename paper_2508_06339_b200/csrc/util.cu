@@ -7,16 +7,58 @@ namespace bsvd {
 __device__ __forceinline__ bool is_finite_v(double v) { return isfinite(v); }
 __device__ __forceinline__ bool is_finite_v(float v) { return isfinite(v); }
 __device__ __forceinline__ bool is_finite_v(__half v) { return isfinite(__half2float(v)); }
+// v * 2^k, exact (sc a power of two; the product stays in range by construction)
+__device__ __forceinline__ double scale_pow2(double v, double sc) { return v * sc; }
+__device__ __forceinline__ float scale_pow2(float v, double sc) { return v * (float)sc; }
+__device__ __forceinline__ __half scale_pow2(__half v, double sc) {
+    return __float2half_rn(__half2float(v) * (float)sc);
+}
 
 // matrix.py:163-181 pad_to_tiles + secondstage.py:518-519 finite check,
 // fused: the padded working copy is written column-major (ld = np) and any
-// NaN/Inf raises a flag the host reads before launching stage 1.
+// NaN/Inf raises a flag the host reads before launching stage 1.  The fast
+// path also normalises each matrix by a power of two (max |a| into [1, 2)):
+// floating-point arithmetic commutes exactly with power-of-two scaling, so
+// ordinary inputs give the same bits, and inputs near the range ends (1e-30,
+// 1e30 in fp32) no longer under/overflow the squared norms of the panel and
+// chase reflectors; the values are multiplied back exactly at the end.
+// Per-matrix max |a| (as the bits of a non-negative double: they order like
+// unsigned integers), for the power-of-two input normalisation.
+template <typename S>
+__global__ void k_absmax(const S *__restrict__ src, int64_t n, int64_t lda, int64_t sbs,
+                         unsigned long long *__restrict__ amax) {
+    const int64_t m = blockIdx.y;
+    src += m * sbs;
+    double mx = 0.0;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = idx / n, r = idx % n;
+        const double v = fabs(to_f64(src[c * lda + r]));
+        mx = v > mx ? v : mx;            // NaN never wins (the finite check reports it)
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax + m, (unsigned long long)__double_as_longlong(mx));
+}
+
+// scale = 2^(1 - e) with max|a| = f 2^e, f in [0.5, 1): max|a| * scale in [1, 2)
+__device__ __forceinline__ double pow2_scale(unsigned long long bits) {
+    const double mx = __longlong_as_double((long long)bits);
+    if (!(mx > 0.0) || !isfinite(mx)) return 1.0;
+    int ex;
+    frexp(mx, &ex);
+    return ldexp(1.0, 1 - ex);
+}
+
 template <typename S>
 __global__ void k_copy_in_pad(const S *__restrict__ src, int64_t n, int64_t lda, int64_t sbs,
-                              S *__restrict__ dst, int64_t np, int *__restrict__ flag) {
+                              S *__restrict__ dst, int64_t np, int *__restrict__ flag,
+                              const unsigned long long *__restrict__ amax, double *__restrict__ unscale) {
     const int64_t m = blockIdx.y;
     src += m * sbs;
     dst += m * np * np;
+    const double sc = amax ? pow2_scale(amax[m]) : 1.0;   // exact: a power of two
+    if (unscale && blockIdx.x == 0 && threadIdx.x == 0) unscale[m] = 1.0 / sc;
     const int64_t total = np * np;
     bool bad = false;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -26,6 +68,7 @@ __global__ void k_copy_in_pad(const S *__restrict__ src, int64_t n, int64_t lda,
         if (r < n && c < n) {
             v = src[c * lda + r];
             bad |= !is_finite_v(v);
+            if (amax) v = scale_pow2(v, sc);
         }
         dst[idx] = v;
     }
@@ -34,13 +77,40 @@ __global__ void k_copy_in_pad(const S *__restrict__ src, int64_t n, int64_t lda,
 
 template <typename S>
 cudaError_t copy_in_pad(const S *src, int64_t n, int64_t lda, int64_t src_bstride, S *dst,
-                        int64_t np, int64_t batch, int *nonfinite_flag, cudaStream_t st) {
+                        int64_t np, int64_t batch, int *nonfinite_flag, cudaStream_t st,
+                        unsigned long long *amax, double *unscale) {
     const int64_t total = np * np;
+    if (amax) {
+        cudaError_t e = cudaMemsetAsync(amax, 0, (size_t)batch * sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        dim3 g1((unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), (unsigned)batch);
+        k_absmax<S><<<g1, 256, 0, st>>>(src, n, lda, src_bstride, amax);
+        bsvd_host::count_launch();
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 8192), (unsigned)batch);
-    k_copy_in_pad<S><<<grid, 256, 0, st>>>(src, n, lda, src_bstride, dst, np, nonfinite_flag);
+    k_copy_in_pad<S><<<grid, 256, 0, st>>>(src, n, lda, src_bstride, dst, np, nonfinite_flag, amax, unscale);
     bsvd_host::count_launch();
     return cudaGetLastError();
 }
+
+// values *= unscale[matrix] (exact powers of two): undo the input normalisation
+template <typename C>
+__global__ void k_unscale_values(C *__restrict__ v, int64_t n, int64_t stride, const double *__restrict__ unscale) {
+    const int64_t m = blockIdx.y;
+    const double u = unscale[m];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[m * stride + i] = (C)((double)v[m * stride + i] * u);
+}
+template <typename C>
+cudaError_t unscale_values(C *v, int64_t n, int64_t stride, int64_t batch, const double *unscale, cudaStream_t st) {
+    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch);
+    k_unscale_values<C><<<grid, 256, 0, st>>>(v, n, stride, unscale);
+    bsvd_host::count_launch();
+    return cudaGetLastError();
+}
+template cudaError_t unscale_values<double>(double *, int64_t, int64_t, int64_t, const double *, cudaStream_t);
+template cudaError_t unscale_values<float>(float *, int64_t, int64_t, int64_t, const double *, cudaStream_t);
 
 // bandreduce.py:113-120 _clear_outside_band.
 template <typename S>
@@ -64,7 +134,8 @@ cudaError_t clear_outside_band(S *a, int64_t n, int bw, int64_t batch, cudaStrea
 
 #define INST(S)                                                                                  \
     template cudaError_t copy_in_pad<S>(const S *, int64_t, int64_t, int64_t, S *, int64_t,       \
-                                        int64_t, int *, cudaStream_t);                           \
+                                        int64_t, int *, cudaStream_t, unsigned long long *,      \
+                                        double *);                                               \
     template cudaError_t clear_outside_band<S>(S *, int64_t, int, int64_t, cudaStream_t);
 INST(double)
 INST(float)

@@ -163,3 +163,49 @@ def test_run_to_run_deterministic(P, torch, n, ts, dtype):
     b = torch.stack([a, a.flip(0)])
     bat = P.svdvals_batched(b, cfg).cpu().numpy()
     assert np.array_equal(bat, P.svdvals_batched(b, cfg).cpu().numpy())
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float16])
+@pytest.mark.parametrize("case", ["zero", "identity", "rank1", "tiny", "huge", "graded"])
+def test_tensor_core_path_edge_inputs(P, oracle, dtype, case):
+    """ts = 128 FP32 / FP16 storage runs the tcgen05 update path: degenerate
+    and badly scaled inputs (exact zeros, identity, rank one, 1e-30 / 1e30
+    scaling within the storage range, a graded spectrum) give the oracle's
+    values within the bound."""
+    n = 384
+    rng = np.random.default_rng(hash(case) % 1000)
+    if case == "zero":
+        a = np.zeros((n, n))
+    elif case == "identity":
+        a = np.eye(n)
+    elif case == "rank1":
+        a = np.outer(rng.standard_normal(n), rng.standard_normal(n))
+    elif case == "tiny":
+        a = rng.standard_normal((n, n)) * (1e-30 if dtype == np.float32 else 1e-3)
+    elif case == "huge":
+        a = rng.standard_normal((n, n)) * (1e30 if dtype == np.float32 else 1e3)
+    else:
+        u, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        a = (u * np.logspace(0, -6, n)) @ v.T
+    a = a.astype(dtype)
+    got = P.svdvals(a, P.KernelConfig(tilesize=128))
+    if case == "zero":
+        assert not np.any(got)
+        return
+    if case == "identity":
+        assert np.array_equal(got, np.ones(n, np.float32))
+        return
+    want = np.linalg.svd(a.astype(np.float64), compute_uv=False)
+    assert_close(got, want, dtype, n, what=f"{case} {np.dtype(dtype).name}")
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float16])
+def test_tensor_core_path_batched(P, oracle, dtype):
+    """Batches on the ts = 128 tensor-core path (blockIdx.z = member, one TMA
+    map with a batch dimension), ragged n (zero padding to 128)."""
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((3, 300, 300)).astype(dtype)
+    got = P.svdvals_batched(a, P.KernelConfig(tilesize=128))
+    for i in range(3):
+        assert_close(got[i], oracle.svdvals(a[i].T.copy(), 128), dtype, 300, what=f"member {i}")
