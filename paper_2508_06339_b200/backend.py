@@ -14,6 +14,7 @@ kernels.py:233-361), so the reference's own driver (``bandsvd.banddiag`` /
 from __future__ import annotations
 
 import contextlib
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -54,7 +55,7 @@ class B200Backend:
         self.stage1 = stage1
         self.stream = stream
         self.stats = LaunchStats()
-        self._ws = None
+        self._tls = threading.local()   # workspace per host thread: concurrent calls never share it
         _lib.load()
 
     # ---- plumbing -------------------------------------------------------
@@ -94,13 +95,17 @@ class B200Backend:
             cur.wait_stream(self.stream)
 
     def workspace(self, nbytes: int):
-        """Cached device scratch (grown on demand; stream-ordered reuse)."""
+        """Cached device scratch of the calling host thread (grown on demand;
+        stream-ordered reuse).  Per thread, so svdvals may be called
+        concurrently on disjoint matrices."""
         import torch
         nbytes = max(int(nbytes), 256)
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = None
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        return self._ws
+        ws = getattr(self._tls, "ws", None)
+        if ws is None or ws.numel() < nbytes:
+            self._tls.ws = None
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._tls.ws = ws
+        return ws
 
     # ---- reference backend protocol ------------------------------------
     def alloc_array(self, size, dtype) -> np.ndarray:
@@ -193,7 +198,7 @@ class B200Backend:
         return self.stats.delta_since(before)
 
     def close(self):
-        self._ws = None
+        self._tls = threading.local()
 
     def __enter__(self):
         return self

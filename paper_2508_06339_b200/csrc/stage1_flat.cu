@@ -1609,6 +1609,7 @@ __global__ void k_zero_cnt(float *ws0, int64_t ws_bstride, int64_t n, int ts, in
 // host side
 
 struct DevCtx {
+    std::mutex enqueue_mu;   // one call's enqueue at a time per device (shared streams/events)
     cudaStream_t sp = nullptr, su = nullptr;
     cudaEvent_t ev[6] = {};
     bool attr_set = false;
@@ -1682,6 +1683,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
     DevCtx *cx = nullptr;
     cudaError_t e = dev_ctx(cx);
     if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> enqueue_lock(cx->enqueue_mu);
     const int64_t N = n / TS;
     const int nsplit = nsplit_for(batch);
     constexpr int W2BM = TS < 64 ? 64 : TS;   // k_fw2x1's tile rows

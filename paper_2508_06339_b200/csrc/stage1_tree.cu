@@ -33,6 +33,9 @@
 
 #include <vector>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_sm100.cuh"
@@ -276,6 +279,41 @@ __device__ void tt_qr(C *Rt, C *Rb, C *tau, C *scal) {
 #include "panel_qr.cuh"
 #include "panel_blocked.cuh"
 namespace bsvd {
+
+// Per-device streams (panel chain at high priority, updates, factors at high
+// priority) and a reusable event pool for the tree stage 1.
+struct TreeCtx {
+    std::mutex mu;
+    cudaStream_t st1 = nullptr, st2 = nullptr, st3 = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaError_t reserve(size_t k) {
+        while (ev.size() < k) {
+            cudaEvent_t e;
+            cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            if (err != cudaSuccess) return err;
+            ev.push_back(e);
+        }
+        return cudaSuccess;
+    }
+};
+static cudaError_t tree_ctx(TreeCtx *&out) {
+    static std::mutex mu;
+    static TreeCtx ctx[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    TreeCtx &c = ctx[dev & 63];
+    if (!c.st2) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if ((e = cudaStreamCreateWithPriority(&c.st1, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&c.st2, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithPriority(&c.st3, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+    }
+    out = &c;
+    return cudaSuccess;
+}
 
 // Development instrumentation (BSVD_PANEL_TRACE): leaf-phase timestamps of
 // one chosen panel launch.
@@ -1141,14 +1179,16 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     if ((err = ensure_smem(k_panel_tt<S, C, TS, DEFER>, psm)) != cudaSuccess) return err;
     if ((err = ensure_smem(k_panel_tt<S, C, TS, false>, psm)) != cudaSuccess) return err;
     if (DEFER && (err = ensure_smem(k_node_tu<C, TS>, NodeTU<C, TS>::smem)) != cudaSuccess) return err;
-    // second stream + events (per call; creation cost is microseconds)
-    cudaStream_t caller = st, st2, st1 = nullptr;
-    if ((err = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    // per-device streams and events, created once and reused by every call
+    // (the enqueue of one call holds the device's lock: calls from several
+    // host threads serialise their enqueue and never share in-flight events)
+    TreeCtx *tcx = nullptr;
+    if ((err = tree_ctx(tcx)) != cudaSuccess) return err;
+    std::lock_guard<std::mutex> enqueue_lock(tcx->mu);
+    cudaStream_t caller = st, st2 = tcx->st2, st1 = nullptr;
     if (!getenv("BSVD_PANEL_NOPRIO")) {       // panel levels on a high-priority stream: the
                                               // critical path gets the next free SM slots
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if ((err = cudaStreamCreateWithPriority(&st1, cudaStreamNonBlocking, hi)) != cudaSuccess) return err;
+        st1 = tcx->st1;
         st = st1;
     }
     // BSVD_S1_TRACE=k: event timeline of sweep side k (RQ) on the three streams
@@ -1166,12 +1206,7 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     // level j (st2) then waits only for its own factors.
     // (high priority: a level's factors must not queue behind the thousands
     // of CTAs of the previous level's update)
-    cudaStream_t st3;
-    {
-        int plo = 0, phi = 0;
-        cudaDeviceGetStreamPriorityRange(&plo, &phi);
-        if ((err = cudaStreamCreateWithPriority(&st3, cudaStreamNonBlocking, phi)) != cudaSuccess) return err;
-    }
+    cudaStream_t st3 = tcx->st3;
     // two-tile leaves (fp32 compute, ts = 128, FMA update path)
     C *ext = ws.nodes + tree_leaf2_offset<C>(N, TS);
     bool leaf2 = false;
@@ -1191,8 +1226,8 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
     bool l2side = false;                                // the current side uses two-tile leaves
     int64_t mtiles = 0;                                 // its panel's tile rows
     const int Lmax0 = tree_levels(N);
-    std::vector<cudaEvent_t> tuev(Lmax0 + 1);
-    for (auto &e : tuev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if ((err = tcx->reserve(2 * (Lmax0 + 1) + 1)) != cudaSuccess) return err;
+    std::vector<cudaEvent_t> tuev(tcx->ev.begin(), tcx->ev.begin() + (Lmax0 + 1));
     std::vector<cudaEvent_t> *lvlp = nullptr;           // set below (panel level events)
     auto level_tu = [&](int j, int64_t slot0, int64_t count, bool tt) -> cudaError_t {
         cudaError_t e2;
@@ -1237,11 +1272,9 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         return e3;
     };
     const int Lmax = tree_levels(N);
-    std::vector<cudaEvent_t> lvl(Lmax + 1);
+    std::vector<cudaEvent_t> lvl(tcx->ev.begin() + (Lmax0 + 1), tcx->ev.begin() + (Lmax0 + 1) + (Lmax + 1));
     lvlp = &lvl;
-    cudaEvent_t done;
-    for (auto &e : lvl) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    cudaEvent_t done = tcx->ev[2 * (Lmax0 + 1)];
     cudaEventRecord(done, caller);             // both start after the caller's queued work
     std::vector<cudaEvent_t> tev;             // timing: (p0, p1) on st, (t0, t1) on st2 per side
     auto tmark = [&](cudaStream_t s) -> cudaEvent_t {
@@ -1379,12 +1412,6 @@ static cudaError_t run_levels(S *a, int64_t n, int64_t batch, int64_t a_bstride,
         }
         for (auto &pe : tl) cudaEventDestroy(pe.second);
     }
-    for (auto &e : lvl) cudaEventDestroy(e);
-    for (auto &e : tuev) cudaEventDestroy(e);
-    cudaEventDestroy(done);
-    cudaStreamDestroy(st2);                    // deferred until its queued work completes
-    cudaStreamDestroy(st3);
-    if (st1) cudaStreamDestroy(st1);
     return err;
 }
 

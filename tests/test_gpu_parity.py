@@ -412,3 +412,25 @@ def test_read_matrix_device_streams_the_file(P, be_tree, tmp_path, dtype):
     got = P.svdvals(t, P.KernelConfig(tilesize=64), backend=be_tree).cpu().numpy()
     want = P.svdvals(read_matrix(path), P.KernelConfig(tilesize=64), backend=be_tree)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dtype,ts", [(np.float32, 128), (np.float64, 64)])
+def test_concurrent_calls_from_threads(P, oracle, dtype, ts):
+    """svdvals is safe to call concurrently on disjoint matrices (SURVEY 8(b),
+    SPEC.md:376): the library's per-device streams and events are shared, and
+    one call's enqueue holds the device lock."""
+    import threading
+    mats = [np.random.default_rng(30 + i).standard_normal((384, 384)).astype(dtype) for i in range(4)]
+    out = [None] * 4
+
+    def work(i):
+        for _ in range(3):
+            out[i] = P.svdvals(mats[i], P.KernelConfig(tilesize=ts))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(4):
+        assert_close(out[i], oracle.svdvals(mats[i], ts), dtype, 384, what=f"thread {i}")
