@@ -16,11 +16,23 @@
 // zero padding adds the smallest ones, matrix.py:163-181), already in the
 // descending order secondstage.py:506 produces with a sort.
 #include <stdlib.h>
+#include <stdio.h>
+
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace bsvd {
+
+#ifndef BSVD_PROBE_ULPS
+#define BSVD_PROBE_ULPS 4.0
+#endif
+constexpr double kProbeUlps = BSVD_PROBE_ULPS;   // first probe offset around Laguerre's iterate
+
+// development instrumentation (BSVD_S3_STATS=file): per value the number of
+// isolation / Laguerre / probe / final-bisection Sturm passes
+__device__ int *g_s3stats = nullptr;
 
 // Per-matrix prep: o2[j] = (o_j * 2^-p)^2, scal = {2^p, gersh_scaled}.
 __global__ void __launch_bounds__(256) k_bisect_prep(const double *__restrict__ d,
@@ -84,6 +96,7 @@ __device__ __forceinline__ double sdiv(double o, double q) {
     return fma(fma(-q, y, o), r, y);
 }
 
+#ifdef BSVD_S3_RATIO
 // #{eigenvalues of TGK < x} for the scaled problem (LAPACK dstebz-style
 // negcount with a pivot floor; zero diagonal so a_j - x = -x).
 __device__ __forceinline__ int negcount(const double *__restrict__ o2, int64_t m, double x,
@@ -144,6 +157,97 @@ __device__ __forceinline__ void negcountK(const double *__restrict__ o2, int64_t
     }
 }
 
+#else
+// Continuant form (default): the leading principal minors
+//   p_0 = 1, p_1 = -x, p_{j+1} = -x p_j - o2_j p_{j-1}
+// of TGK - xI, whose sign changes are the same count as the negative pivots
+// q_j = p_j / p_{j-1} of the ratio form above -- but the dependency chain per
+// step is one FMA instead of a reciprocal, a Newton step and a correction
+// (about 1/6 of the latency; the stage is latency-bound with one value per
+// thread).  Every 8 steps the pair (p_{j-1}, p_j) is rescaled by the power of
+// two that brings its larger magnitude into [1, 2): exact, so signs and the
+// count are unaffected; between rescales |p| grows by at most 12^8 (|x| <= 8,
+// o2 <= 4 after the prep's scaling) and shrinks by at most (2^-120)^8 (x >=
+// floor_), both inside the double range.  Each minor is computed as
+// fma(p_j, 2^-300, -x p_j - o2_j p_{j-1}): the recurrence at x - 2^-300
+// (x >= floor_ = 2^-120 gersh, so far below an ulp of x) -- an exact zero
+// minor becomes 2^-300 p_j, taking its predecessor's sign (the ratio form's
+// q = +pivmin): at x exactly equal to an eigenvalue the count excludes it, so
+// exact inputs still converge to the exact value, and a split (o2_j = 0)
+// after a zero minor cannot stall the recurrence at zero.  Every nonzero
+// minor is unchanged by the second rounding, and the fix costs one dependent
+// FMA instead of a compare and select (61 against 90 cycles per step on
+// B200, scripts/s3_lat.cu).
+__device__ __forceinline__ double cstep(double x, double p, double o, double pm) {
+    return fma(p, 0x1p-300, fma(-x, p, -o * pm));
+}
+// 2^(1023 - e) for the biased exponent e of v: v * pow2_norm(v) in [1, 2)
+__device__ __forceinline__ double pow2_norm(double v) {
+    return __hiloint2double(0x7fe00000 - (__double2hiint(v) & 0x7ff00000), 0);
+}
+
+template <int K>
+__device__ __forceinline__ void negcountK(const double *__restrict__ o2, int64_t m, const double (&x)[K],
+                                          double pivmin, int (&c)[K]) {
+    (void)pivmin;
+    double pm[K], p[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        pm[i] = 1.0;
+        p[i] = fma(1.0, 0x1p-300, -x[i]);
+        c[i] = p[i] < 0.0;
+    }
+    int64_t j = 0;
+    for (; j + 8 <= m; j += 8) {
+        double o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = __ldg(o2 + j + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                const double pn = cstep(x[i], p[i], o[u], pm[i]);
+                c[i] += (pn < 0.0) != (p[i] < 0.0);
+                pm[i] = p[i];
+                p[i] = pn;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const double s = pow2_norm(fmax(fabs(pm[i]), fabs(p[i])));
+            pm[i] *= s;
+            p[i] *= s;
+        }
+    }
+    for (; j < m; ++j) {
+        const double o = __ldg(o2 + j);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const double pn = cstep(x[i], p[i], o, pm[i]);
+            c[i] += (pn < 0.0) != (p[i] < 0.0);
+            pm[i] = p[i];
+            p[i] = pn;
+        }
+    }
+}
+
+__device__ __forceinline__ int negcount(const double *__restrict__ o2, int64_t m, double x, double pivmin) {
+    const double xs[1] = {x};
+    int c[1];
+    negcountK<1>(o2, m, xs, pivmin, c);
+    return c[0];
+}
+
+__device__ __forceinline__ void negcount2(const double *__restrict__ o2, int64_t m, double x0,
+                                          double x1, double pivmin, int &c0, int &c1) {
+    const double xs[2] = {x0, x1};
+    int c[2];
+    negcountK<2>(o2, m, xs, pivmin, c);
+    c0 = c[0];
+    c1 = c[1];
+}
+#endif
+
 // Multisection of the bracket N(lo) < rank <= N(hi) with K points per pass
 // (K interleaved chains in one thread: when values are scarce the stage is
 // latency-bound and K chains cost about one pass of one chain): lo moves to
@@ -190,6 +294,7 @@ __device__ __forceinline__ void multisect(const double *__restrict__ ob, int64_t
     }
 }
 
+#ifdef BSVD_S3_RATIO
 // Sturm count (identical arithmetic to negcount) plus the Laguerre sums at x:
 // G = sum 1/(x - lambda) = (log|f|)', S2 = (log|f|)'' = -sum 1/(x - lambda)^2
 // for f(x) = det(TGK - x I), from the derivative recurrences of
@@ -226,6 +331,44 @@ __device__ __forceinline__ int sturm_laguerre(const double *__restrict__ o2, int
     return cnt;
 }
 
+#else
+// Count plus the Laguerre sums from the continuant and its derivatives
+// (p' and p'' obey the same recurrence with the extra terms -p, -2p'):
+// G = p'/p and S2 = p''/p - G^2 at the end; the 8-step power-of-two rescale
+// multiplies all six carried values alike.
+__device__ __forceinline__ int sturm_laguerre(const double *__restrict__ o2, int64_t m, double x,
+                                              double pivmin, double &G, double &S2) {
+    (void)pivmin;
+    double pm = 1.0, p = fma(1.0, 0x1p-300, -x);
+    double dpm = 0.0, dp = -1.0, ddpm = 0.0, ddp = 0.0;
+    int cnt = p < 0.0;
+    int64_t j = 0;
+    auto step = [&](double o) {
+        const double pn = cstep(x, p, o, pm);
+        const double dpn = fma(-x, dp, fma(-o, dpm, -p));
+        const double ddpn = fma(-x, ddp, fma(-o, ddpm, -2.0 * dp));
+        cnt += (pn < 0.0) != (p < 0.0);
+        pm = p; p = pn;
+        dpm = dp; dp = dpn;
+        ddpm = ddp; ddp = ddpn;
+    };
+    for (; j + 8 <= m; j += 8) {
+        double o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = __ldg(o2 + j + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) step(o[u]);
+        const double s = pow2_norm(fmax(fabs(pm), fabs(p)));
+        pm *= s; p *= s; dpm *= s; dp *= s; ddpm *= s; ddp *= s;
+    }
+    for (; j < m; ++j) step(__ldg(o2 + j));
+    const double r = 1.0 / p;
+    G = dp * r;
+    S2 = fma(ddp, r, -G * G);
+    return cnt;
+}
+#endif
+
 // One value, bracket N(lo) < rank <= N(hi) with counts clo, chi known.  If
 // the bracket isolates the value (chi - clo == 1), Laguerre's iteration for
 // the real-rooted det(TGK - xI) (degree 2n) converges cubically and
@@ -238,12 +381,14 @@ __device__ __forceinline__ double finish_value(const double *__restrict__ ob, in
                                                double lo, double hi, int64_t clo, int64_t chi,
                                                double pivmin, double floor_) {
     const int64_t m = 2 * n - 1;
+    int n_lag = 0, n_probe = 0, n_bis = 0;
     if (chi - clo == 1 && hi > floor_) {
         const double Nd = 2.0 * (double)n;
         double x = 0.5 * (lo + hi);
         bool conv = false;
         for (int it = 0; it < 40; ++it) {
             double G, S2;
+            ++n_lag;
             const int64_t c = sturm_laguerre(ob, m, x, pivmin, G, S2) - n;
             if (c < rank) lo = x; else hi = x;
             if (!(hi - lo > 16.0 * 0x1p-52 * hi)) { conv = true; break; }
@@ -262,11 +407,12 @@ __device__ __forceinline__ double finish_value(const double *__restrict__ ob, in
             x = xn;
         }
         if (conv) {                                   // close the bracket around x
-            double dl = 16.0 * 0x1p-52 * fabs(x) + pivmin;
+            double dl = kProbeUlps * 0x1p-52 * fabs(x) + pivmin;
             for (int rep = 0; rep < 4; ++rep) {
                 const double xl = x - dl, xh = x + dl;
                 const bool inl = xl > lo && xl < hi, inh = xh > lo && xh < hi;
                 int cl = 0, ch = 0;                   // both probes in one pass
+                ++n_probe;
                 if (inl && inh) negcount2(ob, m, xl, xh, pivmin, cl, ch);
                 else if (inl) cl = negcount(ob, m, xl, pivmin);
                 else if (inh) ch = negcount(ob, m, xh, pivmin);
@@ -287,9 +433,14 @@ __device__ __forceinline__ double finish_value(const double *__restrict__ ob, in
         for (int it = 0; it < 200; ++it) {           // bisection to adjacent doubles
             const double mid = 0.5 * (lo + hi);
             if (!(mid > lo && mid < hi) || hi <= floor_) break;
+            ++n_bis;
             const int64_t cnt = negcount(ob, m, mid, pivmin) - n;
             if (cnt < rank) lo = mid; else hi = mid;
         }
+    }
+    if (g_s3stats && blockIdx.y == 0) {
+        int *st = g_s3stats + 4 * (n - rank);
+        st[1] = n_lag; st[2] = n_probe; st[3] = n_bis;
     }
     return lo;
 }
@@ -434,13 +585,15 @@ __global__ void __launch_bounds__(128) k_values(const double *__restrict__ o2,
         if constexpr (K > 1) {
             multisect<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_, true);   // until isolated
         } else {
-            for (int it = 0; it < 64; ++it) {            // bisect until isolated
+            int it = 0;
+            for (; it < 64; ++it) {                      // bisect until isolated
                 if (hi <= floor_ || chi - clo == 1) break;
                 const double mid = 0.5 * (lo + hi);
                 if (!(mid > lo && mid < hi)) break;
                 const int64_t c = negcount(ob, 2 * n - 1, mid, pivmin) - n;
                 if (c < rank) { lo = mid; clo = c; } else { hi = mid; chi = c; }
             }
+            if (g_s3stats && b == 0) g_s3stats[4 * k] = it;
         }
         res = finish_value<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_) * unscale;
     }
@@ -483,17 +636,33 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
         const int vb = getenv("BSVD_VALUES_BLOCK") ? atoi(getenv("BSVD_VALUES_BLOCK"))
                        : (n_out * batch >= 148 * 128 ? 128 : 32);
         // BSVD_VALUES_K=4/8: multisection with K interleaved chains per thread
-        // (same values bit for bit; measured at 8192: K=4 21.0 ms, K=8 69.7 ms
-        // against 20.8 ms for bisection -- the chains do not come for free)
+        // (same values bit for bit; continuant counts at 8192: K=1 8.14 ms,
+        // K=4 7.85 ms, K=8 11.25 ms; 16384: K=1 30.3 ms, K=4 25.1 ms)
         int K = 1;
         if (const char *e = getenv("BSVD_VALUES_K")) K = atoi(e) == 8 ? 8 : (atoi(e) == 4 ? 4 : 1);
         const dim3 vg((unsigned)((n_out + vb - 1) / vb), (unsigned)batch);
+        const char *stats_path = getenv("BSVD_S3_STATS");
+        int *stats = nullptr;
+        if (stats_path) {
+            cudaMalloc(&stats, (size_t)n_out * 4 * sizeof(int));
+            cudaMemset(stats, 0, (size_t)n_out * 4 * sizeof(int));
+            cudaMemcpyToSymbolAsync(g_s3stats, &stats, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
+        }
         if (K == 8)
             k_values<OutT, 8><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
         else if (K == 4)
             k_values<OutT, 4><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
         else
             k_values<OutT, 1><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
+        if (stats) {
+            void *null_ptr = nullptr;
+            cudaMemcpyToSymbolAsync(g_s3stats, &null_ptr, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
+            std::vector<int> h((size_t)n_out * 4);
+            cudaMemcpyAsync(h.data(), stats, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            if (FILE *f = fopen(stats_path, "wb")) { fwrite(h.data(), sizeof(int), h.size(), f); fclose(f); }
+            cudaFree(stats);
+        }
         bsvd_host::count_launch();
         return cudaGetLastError();
     }

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+python scripts/s3_time.py 8192 1 4 8
+python scripts/s3_time.py 4096 1 4 8
+python scripts/s3_time.py 16384 1 4
+python -m pytest tests -m gpu -x -q 2>&1 | tail -4
