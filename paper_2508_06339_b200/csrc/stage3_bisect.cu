@@ -29,10 +29,18 @@ namespace bsvd {
 #define BSVD_PROBE_ULPS 4.0
 #endif
 constexpr double kProbeUlps = BSVD_PROBE_ULPS;   // first probe offset around Laguerre's iterate
+#ifndef BSVD_STENCIL_SIDED
+#define BSVD_STENCIL_SIDED 0
+#endif
+#ifndef BSVD_STENCIL_TRIG
+#define BSVD_STENCIL_TRIG 0x1p-24
+#endif
+constexpr double kStencilTrig = BSVD_STENCIL_TRIG;   // relative Laguerre step that predicts convergence
 
 // development instrumentation (BSVD_S3_STATS=file): per value the number of
 // isolation / Laguerre / probe / final-bisection Sturm passes
 __device__ int *g_s3stats = nullptr;
+__device__ int64_t g_s3trace = -1;   // BSVD_S3_TRACE=k: printf the passes of value k
 
 // Per-matrix prep: o2[j] = (o_j * 2^-p)^2, scal = {2^p, gersh_scaled}.
 __global__ void __launch_bounds__(256) k_bisect_prep(const double *__restrict__ d,
@@ -256,11 +264,12 @@ __device__ __forceinline__ void negcount2(const double *__restrict__ o2, int64_t
 // double lies strictly inside, hi <= floor_, or (isolate) the bracket holds
 // one value.
 template <int K>
-__device__ __forceinline__ void multisect(const double *__restrict__ ob, int64_t n, int64_t rank, double &lo,
+__device__ __forceinline__ int multisect(const double *__restrict__ ob, int64_t n, int64_t rank, double &lo,
                                           double &hi, int64_t &clo, int64_t &chi, double pivmin, double floor_,
                                           bool isolate) {
     const int64_t m = 2 * n - 1;
-    for (int pass = 0; pass < 200; ++pass) {
+    int pass = 0;
+    for (; pass < 200; ++pass) {
         if (hi <= floor_ || (isolate && chi - clo == 1)) break;
         const double w = hi - lo;
         double x[K];
@@ -292,6 +301,7 @@ __device__ __forceinline__ void multisect(const double *__restrict__ ob, int64_t
             if (ok[i] && i > top && c[i] - n >= rank) { nhi = x[i]; nchi = c[i] - n; }
         lo = nlo; hi = nhi; clo = nclo; chi = nchi;
     }
+    return pass;
 }
 
 #ifdef BSVD_S3_RATIO
@@ -367,6 +377,62 @@ __device__ __forceinline__ int sturm_laguerre(const double *__restrict__ o2, int
     S2 = fma(ddp, r, -G * G);
     return cnt;
 }
+
+// One pass: the Laguerre sums and the count at x (as sturm_laguerre) plus
+// Sturm counts at E more points, all chains sharing the o2 stream (with E = 2
+// a pass costs 106 cycles per step against 100 for sturm_laguerre alone and
+// 66 for one count, scripts/s3_lat2.cu).
+template <int E>
+__device__ __forceinline__ int sturm_laguerre_pts(const double *__restrict__ o2, int64_t m, double x,
+                                                  const double (&xs)[E], double &G, double &S2, int (&c)[E]) {
+    double qm[E], q[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        qm[i] = 1.0;
+        q[i] = fma(1.0, 0x1p-300, -xs[i]);
+        c[i] = q[i] < 0.0;
+    }
+    double pm = 1.0, p = fma(1.0, 0x1p-300, -x);
+    double dpm = 0.0, dp = -1.0, ddpm = 0.0, ddp = 0.0;
+    int cnt = p < 0.0;
+    auto step = [&](double o) {
+        const double pn = cstep(x, p, o, pm);
+        const double dpn = fma(-x, dp, fma(-o, dpm, -p));
+        const double ddpn = fma(-x, ddp, fma(-o, ddpm, -2.0 * dp));
+        cnt += (pn < 0.0) != (p < 0.0);
+        pm = p; p = pn;
+        dpm = dp; dp = dpn;
+        ddpm = ddp; ddp = ddpn;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const double qn = cstep(xs[i], q[i], o, qm[i]);
+            c[i] += (qn < 0.0) != (q[i] < 0.0);
+            qm[i] = q[i];
+            q[i] = qn;
+        }
+    };
+    int64_t j = 0;
+    for (; j + 8 <= m; j += 8) {
+        double o[8];
+#pragma unroll
+        for (int u8 = 0; u8 < 8; ++u8) o[u8] = __ldg(o2 + j + u8);
+#pragma unroll
+        for (int u8 = 0; u8 < 8; ++u8) step(o[u8]);
+        const double s = pow2_norm(fmax(fabs(pm), fabs(p)));
+        pm *= s; p *= s; dpm *= s; dp *= s; ddpm *= s; ddp *= s;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const double si = pow2_norm(fmax(fabs(qm[i]), fabs(q[i])));
+            qm[i] *= si;
+            q[i] *= si;
+        }
+    }
+    for (; j < m; ++j) step(__ldg(o2 + j));
+    const double r = 1.0 / p;
+    G = dp * r;
+    S2 = fma(ddp, r, -G * G);
+    return cnt;
+}
 #endif
 
 // One value, bracket N(lo) < rank <= N(hi) with counts clo, chi known.  If
@@ -428,7 +494,7 @@ __device__ __forceinline__ double finish_value(const double *__restrict__ ob, in
         }
     }
     if constexpr (K > 1) {                           // multisection to adjacent doubles
-        multisect<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_, false);
+        n_bis = multisect<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_, false);
     } else {
         for (int it = 0; it < 200; ++it) {           // bisection to adjacent doubles
             const double mid = 0.5 * (lo + hi);
@@ -439,7 +505,7 @@ __device__ __forceinline__ double finish_value(const double *__restrict__ ob, in
         }
     }
     if (g_s3stats && blockIdx.y == 0) {
-        int *st = g_s3stats + 4 * (n - rank);
+        int *st = g_s3stats + 8 * (n - rank);
         st[1] = n_lag; st[2] = n_probe; st[3] = n_bis;
     }
     return lo;
@@ -583,7 +649,8 @@ __global__ void __launch_bounds__(128) k_values(const double *__restrict__ o2,
             lo = 0.0; hi = 2.0 * gersh; clo = 0; chi = n;
         }
         if constexpr (K > 1) {
-            multisect<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_, true);   // until isolated
+            const int it = multisect<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_, true);   // until isolated
+            if (g_s3stats && b == 0) g_s3stats[8 * k] = it;
         } else {
             int it = 0;
             for (; it < 64; ++it) {                      // bisect until isolated
@@ -593,12 +660,159 @@ __global__ void __launch_bounds__(128) k_values(const double *__restrict__ o2,
                 const int64_t c = negcount(ob, 2 * n - 1, mid, pivmin) - n;
                 if (c < rank) { lo = mid; clo = c; } else { hi = mid; chi = c; }
             }
-            if (g_s3stats && b == 0) g_s3stats[4 * k] = it;
+            if (g_s3stats && b == 0) g_s3stats[8 * k] = it;
         }
         res = finish_value<K>(ob, n, rank, lo, hi, clo, chi, pivmin, floor_) * unscale;
     }
     out[b * out_stride + k] = (OutT)res;
 }
+
+#ifndef BSVD_S3_RATIO
+// One thread per value, every pass the SAME code for every lane (a warp's
+// lanes otherwise serialise their different phases): the Laguerre sums at a
+// point xc plus counts at xa < xc < xb (sturm_laguerre_pts<2>).  Per lane:
+//  * not isolated (or Laguerre given up): xa, xc, xb quarter the bracket;
+//  * isolated: xc = Laguerre's iterate (the cell midpoint first), xa, xb =
+//    xc -+ delta with delta = one ulp once the last step predicts xc within
+//    rounding of the value (cubic convergence: relative step < 2^-18), else
+//    xc itself (no extra information).  The ulp stencil
+//    brackets the value between adjacent doubles in the same pass that
+//    evaluates the converged iterate, so no separate probe or bisection
+//    passes follow.
+// Every count keeps N(lo) < rank <= N(hi); a lane is done when lo and hi are
+// adjacent doubles (or hi <= floor_), i.e. at the value plain bisection
+// returns.
+template <typename OutT>
+__global__ void __launch_bounds__(128) k_values_u(const double *__restrict__ o2,
+                                                  const double *__restrict__ scal,
+                                                  const int *__restrict__ cnt, int P, int64_t n,
+                                                  int64_t n_out, OutT *__restrict__ out,
+                                                  int64_t out_stride) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const double *ob = o2 + b * (2 * n - 1);
+    const int *cb = cnt + b * (int64_t)(P + 1);
+    const double unscale = scal[2 * b], gersh = scal[2 * b + 1];
+    if (!(gersh > 0.0)) {
+        if (k < n_out) out[b * out_stride + k] = (OutT)0.0;
+        return;
+    }
+    const int64_t m = 2 * n - 1;
+    const int64_t rank = n - (k < n_out ? k : n_out - 1);
+    const double floor_ = 0x1p-120 * gersh;
+    const double h = 2.0 * gersh / P;
+    int lo_p = 0, hi_p = P;                              // cb[lo_p] < rank <= cb[hi_p]
+    while (hi_p - lo_p > 1) {
+        const int mid = (lo_p + hi_p) >> 1;
+        if (__ldg(cb + mid) < rank) lo_p = mid; else hi_p = mid;
+    }
+    double lo = lo_p * h, hi = hi_p < P ? hi_p * h : 2.0 * gersh;
+    int64_t clo = __ldg(cb + lo_p), chi = __ldg(cb + hi_p);
+    if (!(clo < rank && rank <= chi)) {                  // non-monotone counts: full range
+        lo = 0.0; hi = 2.0 * gersh; clo = 0; chi = n;
+    }
+    const double Nd = 2.0 * (double)n;
+    bool done = k >= n_out || hi <= floor_;
+    bool lag_ok = true;                                  // Laguerre not given up
+    bool above = true;       // the value lies below the iterate (Laguerre keeps the side)
+    double x = 0.5 * (lo + hi), sprev = 1.0;
+    int n_pass = 0, n_lag = 0, n_fail = 0;
+    for (int it = 0; it < 400; ++it) {
+        if (!__any_sync(0xffffffffu, !done)) break;
+        const bool lag = !done && lag_ok && chi - clo == 1;
+        const bool stencil = lag && sprev < kStencilTrig;
+        double u = 0.0;
+        double px[3];                                    // ascending; px[ic] is the Laguerre point
+        int ic = 1;
+        if (done) {
+            px[0] = px[1] = px[2] = hi;
+        } else if (lag) {
+            u = __hiloint2double((__double2hiint(fabs(x)) & 0x7ff00000) - (52 << 20), 0);
+            // once converged, two more doubles on the value's side of the
+            // iterate; before that no extra information (a point between the
+            // iterate and the value would push Laguerre's step outside the bracket)
+            const double d = stencil ? u : 0.0;
+#if BSVD_STENCIL_SIDED
+            if (above) { px[0] = x - 2.0 * d; px[1] = x - d; px[2] = x; ic = 2; }
+            else       { px[0] = x; px[1] = x + d; px[2] = x + 2.0 * d; ic = 0; }
+#else
+            px[0] = x - d; px[1] = x; px[2] = x + d;
+#endif
+        } else {
+            const double w = hi - lo;
+            px[0] = lo + 0.25 * w;
+            px[1] = lo + 0.5 * w;
+            px[2] = lo + 0.75 * w;
+        }
+        const double xc = px[ic];
+        const double xs[2] = {px[ic == 0 ? 1 : 0], px[ic == 2 ? 1 : 2]};
+        double G, S2;
+        int cs[2];
+        const int64_t cc = sturm_laguerre_pts<2>(ob, m, xc, xs, G, S2, cs) - n;
+        if (done) continue;
+        ++n_pass;
+        n_lag += lag;
+        int64_t pc[3];
+        pc[ic] = cc;
+        pc[ic == 0 ? 1 : 0] = cs[0] - n;
+        pc[ic == 2 ? 1 : 2] = cs[1] - n;
+        // lo -> the highest point inside (lo, hi) with N < rank, hi -> the
+        // lowest point above it with N >= rank (robust to non-monotone counts)
+        int top = -1;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            if (px[i] > lo && px[i] < hi && pc[i] < rank) top = i;
+        double nlo = lo, nhi = hi;
+        int64_t nclo = clo, nchi = chi;
+        if (top >= 0) { nlo = px[top]; nclo = pc[top]; }
+#pragma unroll
+        for (int i = 2; i >= 0; --i)
+            if (i > top && px[i] > lo && px[i] < hi && pc[i] >= rank) { nhi = px[i]; nchi = pc[i]; }
+        lo = nlo; hi = nhi; clo = nclo; chi = nchi;
+        if (k == g_s3trace && b == 0)
+            printf("pass %d lag %d st %d xc %.17g cc %lld (rank %lld) lo %.17g hi %.17g w/ulp %.3g G %.6g S2 %.6g sprev %.3g\n",
+                   n_pass, (int)lag, (int)stencil, xc, (long long)cc, (long long)rank, lo, hi,
+                   (hi - lo) / (0x1p-52 * fabs(hi)), G, S2, sprev);
+        const double mid = 0.5 * (lo + hi);
+        if (hi <= floor_ || !(mid > lo && mid < hi)) { done = true; continue; }
+        if (lag) {
+            above = cc >= rank;
+            const double H = -S2;
+            double disc = (Nd - 1.0) * (Nd * H - G * G);
+            disc = disc > 0.0 ? disc : 0.0;
+            const double sq = sqrt(disc);
+            const double xa = xc - Nd / (G + sq), xb = xc - Nd / (G - sq);
+            double xn = above ? fmin(xa, xb) : fmax(xa, xb);
+            const double stp = fabs(xn - xc) / fabs(xc);
+            if (stencil) {
+                // the stencil missed: the value is more than two doubles away
+                // on its side.  A step from a point that close is rounding
+                // noise in G, S2 when it is large: walk three doubles instead.
+                if (++n_fail >= 4) lag_ok = false;
+                if (stp > 0x1p-18) xn = above ? xc - 3.0 * u : xc + 3.0 * u;
+            }
+            sprev = stp <= 64.0 * 0x1p-52 ? 0.0 : stp;
+            if (n_lag >= 16) lag_ok = false;
+            // a step onto or past a bound (the value within rounding of it):
+            // the double next to that bound
+            if (!(xn < hi)) xn = hi - __hiloint2double((__double2hiint(hi) & 0x7ff00000) - (52 << 20), 0);
+            if (!(xn > lo)) xn = lo + __hiloint2double((__double2hiint(fabs(lo)) & 0x7ff00000) - (52 << 20), 0);
+            if (!(xn > lo && xn < hi)) xn = mid;
+            x = xn;
+        } else if (lag_ok && chi - clo == 1) {
+            x = mid;                                     // just isolated: Laguerre from the midpoint
+            sprev = 1.0;
+        }
+    }
+    if (k < n_out) {
+        out[b * out_stride + k] = (OutT)(lo * unscale);
+        if (g_s3stats && b == 0) {
+            int *st = g_s3stats + 8 * k;
+            st[0] = n_pass - n_lag; st[1] = n_lag; st[6] = n_fail; st[7] = lag_ok;
+        }
+    }
+}
+#endif
 
 static int slice_points(int64_t n) {
     static const int per = getenv("BSVD_SLICE_PER") ? atoi(getenv("BSVD_SLICE_PER")) : 4;
@@ -641,13 +855,23 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
         int K = 1;
         if (const char *e = getenv("BSVD_VALUES_K")) K = atoi(e) == 8 ? 8 : (atoi(e) == 4 ? 4 : 1);
         const dim3 vg((unsigned)((n_out + vb - 1) / vb), (unsigned)batch);
+        if (const char *tr = getenv("BSVD_S3_TRACE")) {
+            const int64_t tk = atoll(tr);
+            cudaMemcpyToSymbolAsync(g_s3trace, &tk, sizeof(tk), 0, cudaMemcpyHostToDevice, st);
+        }
         const char *stats_path = getenv("BSVD_S3_STATS");
         int *stats = nullptr;
         if (stats_path) {
-            cudaMalloc(&stats, (size_t)n_out * 4 * sizeof(int));
-            cudaMemset(stats, 0, (size_t)n_out * 4 * sizeof(int));
+            cudaMalloc(&stats, (size_t)n_out * 8 * sizeof(int));
+            cudaMemset(stats, 0, (size_t)n_out * 8 * sizeof(int));
             cudaMemcpyToSymbolAsync(g_s3stats, &stats, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
         }
+        static const bool legacy = getenv("BSVD_VALUES_LEGACY") != nullptr;
+#ifndef BSVD_S3_RATIO
+        if (!legacy && !getenv("BSVD_VALUES_K"))
+            k_values_u<OutT><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
+        else
+#endif
         if (K == 8)
             k_values<OutT, 8><<<vg, vb, 0, st>>>(o2, scal, cnt, P, n, n_out, out, out_stride);
         else if (K == 4)
@@ -657,7 +881,7 @@ cudaError_t bidiagonal_values(const double *d, const double *e, int64_t n, int64
         if (stats) {
             void *null_ptr = nullptr;
             cudaMemcpyToSymbolAsync(g_s3stats, &null_ptr, sizeof(void *), 0, cudaMemcpyHostToDevice, st);
-            std::vector<int> h((size_t)n_out * 4);
+            std::vector<int> h((size_t)n_out * 8);
             cudaMemcpyAsync(h.data(), stats, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
             if (FILE *f = fopen(stats_path, "wb")) { fwrite(h.data(), sizeof(int), h.size(), f); fclose(f); }

@@ -12,7 +12,10 @@ ks = sys.argv[2:] or [os.environ.get("BSVD_VALUES_K", "1")]
 a = torch.randn(n, n, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
 first = None
 for k in ks:
-    os.environ["BSVD_VALUES_K"] = k
+    if k == "u":
+        os.environ.pop("BSVD_VALUES_K", None)
+    else:
+        os.environ["BSVD_VALUES_K"] = k
     v = P.svdvals(a)
     ts = []
     for _ in range(7):
