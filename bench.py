@@ -353,7 +353,7 @@ def run_b200(args):
                                                       2 if dtype == torch.float16 else 4) * units
     s1_traffic = traffic.get(f"stage1_step_n{n}") if wl == "single" else None
     phases = {
-        "stage1": {"bound": "fma", "achieved": ach1, "peak": fpk, "unit": "TFLOP/s", "frac": ach1 / fpk,
+        "stage1": {"bound": "fma", "ms": stage1_ms, "achieved": ach1, "peak": fpk, "unit": "TFLOP/s", "frac": ach1 / fpk,
                    "kernel": ("stage 1: k_fpanel2 (cluster Householder panel) + k_tgemm (tcgen05 3xTF32 W = V^T X "
                               "and X -= V W2, TMA-fed) + k_tbuild + k_fw2x1" if tc_on else
                               "stage 1: k_fpanel2 + k_fgemm1/k_fgemm2 (FMA) + k_fgram + k_fw2x1"),
@@ -373,7 +373,7 @@ def run_b200(args):
         chase_k, chase_d = "k_chase_cta", "k_chase_cta (stage 2, one CTA per matrix, carried blocks in registers)"
     else:
         chase_k, chase_d = "k_chase", "k_chase (stage 2, pipelined cluster chase)"
-    phases["bidiagonal"] = {"bound": "hbm", "kernel": chase_d,
+    phases["bidiagonal"] = {"bound": "hbm", "kernel": chase_d, "ms": per["bidiagonal"],
                             "achieved": ach2, "peak": hbm_gbs, "unit": "GB/s", "frac": ach2 / hbm_gbs,
                             "peak_source": peak_src, "algorithmic_bytes": algo_bytes,
                             "model": f"touch model 2*bw*n^2*{belem} B per matrix (SURVEY.md 8(d)); the band "
@@ -382,7 +382,7 @@ def run_b200(args):
                             "traffic": traffic.get(chase_k) if wl == "single" else None}
     # stage 3: the number of Sturm passes per value is data dependent; no flop
     # model -- time only
-    phases["diagonal"] = {"bound": "latency", "kernel": "k_slice + k_values (stage 3, fp64 Sturm counts)",
+    phases["diagonal"] = {"bound": "latency", "kernel": "k_slice + k_values_u (stage 3, fp64 continuant Sturm counts + Laguerre)",
                           "ms": per["diagonal"], "achieved": None, "peak": None, "frac": None,
                           "traffic": traffic.get("k_values") if wl == "single" else None}
     # the required roofline object: the largest single kernel of the step (the

@@ -1613,6 +1613,7 @@ struct DevCtx {
     cudaStream_t sp = nullptr, su = nullptr;
     cudaEvent_t ev[6] = {};
     bool attr_set = false;
+    int nsm = 148;
 };
 static std::mutex g_mu;
 static DevCtx g_ctx[64];
@@ -1630,6 +1631,7 @@ static cudaError_t dev_ctx(DevCtx *&out) {
         if ((e = cudaStreamCreateWithFlags(&c.su, cudaStreamNonBlocking)) != cudaSuccess) return e;
         for (auto &ev : c.ev)
             if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+        cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     out = &c;
     return cudaSuccess;
@@ -1785,7 +1787,13 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
             // W partials over row splits
             const int cblk = (C + 127) / 128;
             int ns = 1;
-            if (batch == 1) {
+            if (batch == 1 && tc1) {
+                // one wave: (cblk + 1 Gram tile) x ns CTAs at one CTA per SM
+                // (a second, partial wave doubles the product's time)
+                ns = std::max(1, std::min(nsplit, cx->nsm / (cblk + 1)));
+                ns = std::min(ns, std::max(1, M / 256));
+                if (getenv("BSVD_TC_NS")) ns = std::max(1, std::min(nsplit, std::min(M / 32, atoi(getenv("BSVD_TC_NS")))));
+            } else if (batch == 1) {
                 ns = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, ((tc1 ? 1 : 2) * 148 + cblk - 1) / cblk));
                 ns = std::min(ns, std::max(1, M / 256));
                 if (tc1 && getenv("BSVD_TC_NS")) ns = std::max(1, std::min(nsplit, std::min(M / 32, atoi(getenv("BSVD_TC_NS")))));

@@ -715,11 +715,12 @@ __global__ void __launch_bounds__(128) k_values_u(const double *__restrict__ o2,
     bool done = k >= n_out || hi <= floor_;
     bool lag_ok = true;                                  // Laguerre not given up
     bool above = true;       // the value lies below the iterate (Laguerre keeps the side)
-    double x = 0.5 * (lo + hi), sprev = 1.0;
+    bool hunt = false;       // geometric search out from the bracket end next to the value
+    double x = 0.5 * (lo + hi), sprev = 1.0, hd = 0.0;
     int n_pass = 0, n_lag = 0, n_fail = 0;
     for (int it = 0; it < 400; ++it) {
         if (!__any_sync(0xffffffffu, !done)) break;
-        const bool lag = !done && lag_ok && chi - clo == 1;
+        const bool lag = !done && !hunt && lag_ok && chi - clo == 1;
         const bool stencil = lag && sprev < kStencilTrig;
         double u = 0.0;
         double px[3];                                    // ascending; px[ic] is the Laguerre point
@@ -738,6 +739,12 @@ __global__ void __launch_bounds__(128) k_values_u(const double *__restrict__ o2,
 #else
             px[0] = x - d; px[1] = x; px[2] = x + d;
 #endif
+        } else if (hunt) {
+            // the value is within a few doubles of the end B next to it (a
+            // converged Laguerre iterate that the stencil missed): B -+ hd,
+            // 4 hd, 16 hd; a wider gap multiplies hd by 64 for the next pass
+            if (above) { px[0] = hi - 16.0 * hd; px[1] = hi - 4.0 * hd; px[2] = hi - hd; }
+            else       { px[0] = lo + hd; px[1] = lo + 4.0 * hd; px[2] = lo + 16.0 * hd; }
         } else {
             const double w = hi - lo;
             px[0] = lo + 0.25 * w;
@@ -784,21 +791,30 @@ __global__ void __launch_bounds__(128) k_values_u(const double *__restrict__ o2,
             const double xa = xc - Nd / (G + sq), xb = xc - Nd / (G - sq);
             double xn = above ? fmin(xa, xb) : fmax(xa, xb);
             const double stp = fabs(xn - xc) / fabs(xc);
-            if (stencil) {
-                // the stencil missed: the value is more than two doubles away
-                // on its side.  A step from a point that close is rounding
-                // noise in G, S2 when it is large: walk three doubles instead.
-                if (++n_fail >= 4) lag_ok = false;
-                if (stp > 0x1p-18) xn = above ? xc - 3.0 * u : xc + 3.0 * u;
-            }
             sprev = stp <= 64.0 * 0x1p-52 ? 0.0 : stp;
-            if (n_lag >= 16) lag_ok = false;
+            if (stencil) {
+                // the stencil missed: the value is more than a double away on
+                // its side.  A large step from a point that close is rounding
+                // noise in G, S2: walk three doubles instead.  A second miss
+                // (Laguerre creeping a few doubles per pass) hunts from the
+                // bracket end next to the value
+                if (stp > 0x1p-18) xn = above ? xc - 3.0 * u : xc + 3.0 * u;
+                if (++n_fail >= 2) { hunt = true; hd = u; lag_ok = false; }
+            }
+            if (n_lag >= 16) { hunt = true; hd = u; lag_ok = false; }
             // a step onto or past a bound (the value within rounding of it):
             // the double next to that bound
             if (!(xn < hi)) xn = hi - __hiloint2double((__double2hiint(hi) & 0x7ff00000) - (52 << 20), 0);
             if (!(xn > lo)) xn = lo + __hiloint2double((__double2hiint(fabs(lo)) & 0x7ff00000) - (52 << 20), 0);
             if (!(xn > lo && xn < hi)) xn = mid;
             x = xn;
+        } else if (hunt) {
+            if (hi - lo <= 16.5 * hd) {
+                // found: quartering finishes the bracket (<= 16 hd)
+                hunt = false;                            // (lag_ok stays false)
+            } else {
+                hd *= 64.0;
+            }
         } else if (lag_ok && chi - clo == 1) {
             x = mid;                                     // just isolated: Laguerre from the midpoint
             sprev = 1.0;
@@ -808,7 +824,7 @@ __global__ void __launch_bounds__(128) k_values_u(const double *__restrict__ o2,
         out[b * out_stride + k] = (OutT)(lo * unscale);
         if (g_s3stats && b == 0) {
             int *st = g_s3stats + 8 * k;
-            st[0] = n_pass - n_lag; st[1] = n_lag; st[6] = n_fail; st[7] = lag_ok;
+            st[0] = n_pass - n_lag; st[1] = n_lag; st[6] = n_fail; st[7] = lag_ok;   // hunt passes count as [0]
         }
     }
 }
