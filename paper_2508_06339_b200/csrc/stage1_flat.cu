@@ -1610,8 +1610,8 @@ __global__ void k_zero_cnt(float *ws0, int64_t ws_bstride, int64_t n, int ts, in
 
 struct DevCtx {
     std::mutex enqueue_mu;   // one call's enqueue at a time per device (shared streams/events)
-    cudaStream_t sp = nullptr, su = nullptr;
-    cudaEvent_t ev[6] = {};
+    cudaStream_t sp = nullptr, su = nullptr, sg = nullptr;
+    cudaEvent_t ev[8] = {};
     bool attr_set = false;
     int nsm = 148;
 };
@@ -1629,6 +1629,7 @@ static cudaError_t dev_ctx(DevCtx *&out) {
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         if ((e = cudaStreamCreateWithPriority(&c.sp, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&c.su, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithPriority(&c.sg, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
         for (auto &ev : c.ev)
             if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
         cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1690,9 +1691,9 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
     const int nsplit = nsplit_for(batch);
     constexpr int W2BM = TS < 64 ? 64 : TS;   // k_fw2x1's tile rows
     const int64_t wsb = (int64_t)ws_floats(n, TS, nsplit);
-    cudaStream_t sp = cx->sp, su = cx->su;
+    cudaStream_t sp = cx->sp, su = cx->su, sg = cx->sg;
     cudaEvent_t evStart = cx->ev[0], evP = cx->ev[1], ev1 = cx->ev[2], evW = cx->ev[3], evEndP = cx->ev[4],
-                evEndU = cx->ev[5];
+                evEndU = cx->ev[5], evT = cx->ev[6], evEndG = cx->ev[7];
     {   // (function attributes are per device: set before every stage)
         e = cudaFuncSetAttribute(k_fw2x1<S, TS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(W2BM * (64 + 4) * sizeof(float)));
@@ -1711,6 +1712,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
     cudaEventRecord(evStart, st);
     cudaStreamWaitEvent(sp, evStart, 0);
     cudaStreamWaitEvent(su, evStart, 0);
+    cudaStreamWaitEvent(sg, evStart, 0);
     cudaEvent_t tp0 = nullptr, tp1 = nullptr;
     if (timed) {
         cudaEventCreate(&tp0);
@@ -1787,10 +1789,16 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
             // W partials over row splits
             const int cblk = (C + 127) / 128;
             int ns = 1;
+            // single matrices: the Gram matrix G = V^T V gets its own ng-way
+            // split launch on the third stream, and k_tbuild forms T from it
+            // while the W tiles are still running -- off the critical path
+            const bool gsep = tc1 && batch == 1 && !getenv("BSVD_GRAM_JOINT");
+            const int ng = gsep ? std::max(1, std::min(std::min(nsplit, 8), M / 512)) : 0;
             if (batch == 1 && tc1) {
-                // one wave: (cblk + 1 Gram tile) x ns CTAs at one CTA per SM
-                // (a second, partial wave doubles the product's time)
-                ns = std::max(1, std::min(nsplit, cx->nsm / (cblk + 1)));
+                // one wave: (cblk W tiles + the Gram tiles) x ns CTAs at one CTA
+                // per SM (a second, partial wave doubles the product's time)
+                ns = gsep ? std::max(1, std::min(nsplit, (cx->nsm - ng) / cblk))
+                          : std::max(1, std::min(nsplit, cx->nsm / (cblk + 1)));
                 ns = std::min(ns, std::max(1, M / 256));
                 if (getenv("BSVD_TC_NS")) ns = std::max(1, std::min(nsplit, std::min(M / 32, atoi(getenv("BSVD_TC_NS")))));
             } else if (batch == 1) {
@@ -1801,7 +1809,23 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
             const int rps = ((M + ns - 1) / ns + (tc1 ? 31 : KC - 1)) / (tc1 ? 32 : KC) * (tc1 ? 32 : KC);
             cudaStreamWaitEvent(su, evP, 0);
             Ws w0 = ws_carve(ws, n, TS, nsplit);
-            if (tc1)
+            if (gsep) {
+                const int rpg = ((M + std::max(ng, 1) - 1) / std::max(ng, 1) + 31) / 32 * 32;
+                cudaStreamWaitEvent(sg, evP, 0);
+                e2 = launch_flat_tc(tcp, par, 3, lq, M, 0, (int)(top * TS), (int)((k + 1) * TS), w0.Wp, w0.Gp, wsb, ng,
+                                    rpg, a, n, a_bstride, batch, sg);
+                if (e2 == cudaSuccess) {
+                    if constexpr (TS == 128) {
+                        k_tbuild<TS><<<(unsigned)batch, kTB, tbuild_smem, sg>>>(ws, wsb, n, nsplit, ng);
+                        bsvd_host::count_launch();
+                        e2 = cudaGetLastError();
+                    }
+                }
+                cudaEventRecord(evT, sg);
+                if (e2 == cudaSuccess)
+                    e2 = launch_flat_tc(tcp, par, 4, lq, M, C, (int)(top * TS), (int)((k + 1) * TS), w0.Wp, w0.Gp, wsb,
+                                        ns, rps, a, n, a_bstride, batch, su);
+            } else if (tc1)
             {
                 e2 = launch_flat_tc(tcp, par, 1, lq, M, C, (int)(top * TS), (int)((k + 1) * TS), w0.Wp, w0.Gp, wsb, ns,
                                     rps, a, n, a_bstride, batch, su);
@@ -1826,6 +1850,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
             if (e2 != cudaSuccess) return e2;
             cudaEventRecord(ev1, su);
             cudaStreamWaitEvent(sp, ev1, 0);
+            if (gsep) cudaStreamWaitEvent(sp, evT, 0);
             const size_t w2sm = W2BM * (64 + 4) * sizeof(float);
             if (lq)
                 k_fw2x1<S, TS, false><<<dim3((unsigned)((C + 63) / 64), 1, (unsigned)batch), kGT, w2sm, sp>>>(
@@ -1863,8 +1888,10 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
     if (e == cudaSuccess) e = side(N - 1, false);
     cudaEventRecord(evEndP, sp);
     cudaEventRecord(evEndU, su);
+    cudaEventRecord(evEndG, sg);
     cudaStreamWaitEvent(st, evEndP, 0);
     cudaStreamWaitEvent(st, evEndU, 0);
+    cudaStreamWaitEvent(st, evEndG, 0);
     if (timed) {
         cudaEventRecord(tp1, st);
         cudaEventSynchronize(tp1);

@@ -439,8 +439,10 @@ cudaError_t launch_flat_tc(const FlatTcPlan *plan, int par, int mode, bool lq, i
     const Maps &maps = plan->maps[par];
     dim3 grid;
     cudaError_t e;
-    if (mode == 1) {
-        grid = dim3((unsigned)(C / BN + 1), (unsigned)ns, (unsigned)batch);   // + the Gram tile
+    if (mode == 1 || mode == 3 || mode == 4) {
+        // 1: W tiles + the Gram tile; 3: the Gram tile alone (C = 0); 4: W tiles alone
+        grid = dim3((unsigned)(mode == 3 ? 1 : C / BN + (mode == 1 ? 1 : 0)), (unsigned)ns, (unsigned)batch);
+        if (mode == 3) g.C = 0;
         auto kern = plan->half ? (lq ? k_tgemm<1, true, true> : k_tgemm<1, false, true>)
                                : (lq ? k_tgemm<1, true, false> : k_tgemm<1, false, false>);
         if ((e = ensure_smem(kern, Cfg<1>::SMEM)) != cudaSuccess) return e;
