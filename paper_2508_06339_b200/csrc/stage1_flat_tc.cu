@@ -49,7 +49,7 @@ namespace ftc {
 constexpr int TS = 128, BM = 128, BN = 128, KB = 32;
 constexpr int NSW = 8;                       // split / epilogue warps
 constexpr int W_MMA = NSW, W_TMA = NSW + 1;
-constexpr int NTH = (NSW + 2) * 32;
+
 constexpr int IMG = BM * KB;                 // floats per operand image (one K-block, 16 KB)
 constexpr int STAGE = 4 * IMG;               // A_hi, A_lo, B_hi, B_lo
 // Accumulation epochs: the TMEM accumulator restarts from zero every EPK
@@ -62,6 +62,10 @@ constexpr int EPK = 1;
 constexpr int TMEM_COLS = 2 * BN;
 template <int MODE>
 struct Cfg {
+    // G1 (MODE 1): eight more warps drain the TMEM epochs, so the split warps
+    // only split and the tensor pipe is not held up by the drains
+    static constexpr bool SEP = MODE == 1;
+    static constexpr int NTH = (NSW + 2 + (SEP ? NSW : 0)) * 32;
     static constexpr int NST = MODE == 1 ? 3 : 2;
     static constexpr size_t XT = MODE == 2 ? (size_t)BM * BN : 0;   // X tile floats
     static constexpr size_t SMEM = ((size_t)NST * STAGE + XT) * sizeof(float) + 1024;
@@ -120,8 +124,9 @@ __device__ __forceinline__ void split_image(float *hi, float *lo, int t) {
 }
 
 template <int MODE, bool LQ, bool H>
-__global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps maps, const Args g) {
+__global__ void __launch_bounds__(Cfg<MODE>::NTH, 1) k_tgemm(const __grid_constant__ Maps maps, const Args g) {
     using CF = Cfg<MODE>;
+    constexpr bool SEP = CF::SEP;
     constexpr int NST = CF::NST;
     extern __shared__ __align__(1024) unsigned char smraw[];
     float *sm = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
@@ -237,10 +242,11 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
             }
         }
     } else {
-        // ---------------- split warps ----------------
-        const int t = tid;   // 0 .. 255
-        const int q = warp & 3;              // TMEM lane quadrant
-        const int chalf = warp >> 2;         // half of the 128 accumulator columns
+        // ---------------- split warps (and, unless SEP, drain + epilogue) ----
+        const int t = tid;   // 0 .. 255 for the split warps
+        const int q = warp & 3;              // TMEM lane quadrant (hardware: warp % 4)
+        const int chalf = SEP ? (warp - NSW - 2) >> 2 : warp >> 2;   // half of the 128 accumulator columns
+        const bool splitter = warp < NSW, drainer = SEP ? warp >= NSW + 2 : true;
         const int m = q * 32 + lane;         // accumulator row
         const int nep = (nkb + EPK - 1) / EPK;
         float sum[64];
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
             tc::fence_before();
             mbar_arrive(&accempty[ab]);
         };
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < (splitter ? nkb : 0); ++kb) {
             const int st = kb % NST;
             tc::mbar_wait(&loaded[st], (uint32_t)((kb / NST) & 1));
             float *base = sm + st * STAGE;
@@ -322,8 +328,9 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
             mbar_arrive(&full[st]);
             // drain epoch e once the first K-block of epoch e+1 is staged (the
             // MMAs keep running in the other accumulator meanwhile)
-            if (kb % EPK == 0 && kb >= EPK) drain(drained++);
+            if (!SEP && kb % EPK == 0 && kb >= EPK) drain(drained++);
         }
+        if (!drainer) goto done;
         while (drained < nep) drain(drained++);
         // ---------------- epilogue (sum = the accumulated tile row m) ----------
         if (MODE == 2) tc::mbar_wait(&xload, 0);
@@ -353,6 +360,7 @@ __global__ void __launch_bounds__(NTH, 1) k_tgemm(const __grid_constant__ Maps m
             }
         }
     }
+done:
     tc::fence_before();
     __syncthreads();
     if (warp == W_MMA) tc::tmem_free<TMEM_COLS>(tmem);
@@ -446,13 +454,13 @@ cudaError_t launch_flat_tc(const FlatTcPlan *plan, int par, int mode, bool lq, i
         auto kern = plan->half ? (lq ? k_tgemm<1, true, true> : k_tgemm<1, false, true>)
                                : (lq ? k_tgemm<1, true, false> : k_tgemm<1, false, false>);
         if ((e = ensure_smem(kern, Cfg<1>::SMEM)) != cudaSuccess) return e;
-        kern<<<grid, NTH, Cfg<1>::SMEM, st>>>(maps, g);
+        kern<<<grid, Cfg<1>::NTH, Cfg<1>::SMEM, st>>>(maps, g);
     } else {
         grid = dim3((unsigned)((M - TS) / BM), (unsigned)(C / BN), (unsigned)batch);
         auto kern = plan->half ? (lq ? k_tgemm<2, true, true> : k_tgemm<2, false, true>)
                                : (lq ? k_tgemm<2, true, false> : k_tgemm<2, false, false>);
         if ((e = ensure_smem(kern, Cfg<2>::SMEM)) != cudaSuccess) return e;
-        kern<<<grid, NTH, Cfg<2>::SMEM, st>>>(maps, g);
+        kern<<<grid, Cfg<2>::NTH, Cfg<2>::SMEM, st>>>(maps, g);
     }
     bsvd_host::count_launch();
     return cudaGetLastError();
