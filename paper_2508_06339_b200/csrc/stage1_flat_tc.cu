@@ -89,6 +89,7 @@ struct Args {
     int64_t ws_bstride;     // floats
     void *X;                // G2 epilogue: matrix base (member 0), storage type
     int64_t n, a_bstride;   // G2 epilogue: leading dim, batch stride
+    int no_pf;              // development: no L2 prefetch of G1's X boxes
 };
 
 __device__ __forceinline__ void tma3(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2) {
@@ -97,6 +98,13 @@ __device__ __forceinline__ void tma3(void *dst, const CUtensorMap *map, uint64_t
             tc::smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
+}
+// L2 prefetch of one TMA box (no shared memory, no completion)
+__device__ __forceinline__ void tma3_prefetch(const CUtensorMap *map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
 }
 __device__ __forceinline__ void expect_tx(uint64_t *m, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(m)), "r"(bytes)
@@ -173,6 +181,7 @@ __global__ void __launch_bounds__(Cfg<MODE>::NTH, 1) k_tgemm(const __grid_consta
     const uint32_t tmem = tslot;
 
     if (warp == W_TMA) {
+        const bool no_pf = g.no_pf != 0;
         if (lane == 0) {
             if (MODE == 2) {   // the epilogue's X tile, 64 KB, first
                 // RQ: inner = rows (m), outer = cols (n); LQ: inner = cols (m), outer = rows (n)
@@ -181,8 +190,21 @@ __global__ void __launch_bounds__(Cfg<MODE>::NTH, 1) k_tgemm(const __grid_consta
                 expect_tx(&xload, (uint32_t)(BM * BN * (H ? 2 : 4)));
                 tma3(xt, &maps.Xt, &xload, inner, outer, b);
             }
+            // G1 streams X from HBM: the smem ring (3 stages) covers less than
+            // the DRAM latency at the MMA rate, so the X boxes PF K-blocks
+            // ahead are prefetched into L2 first
+            constexpr int PF = 8;
+            auto prefetch_x = [&](int kb) {
+                if (MODE != 1 || gtile || kb >= nkb) return;
+                const int kk = kb * KB;
+                if (!LQ) tma3_prefetch(&maps.Xk, g.row_base + k_lo + kk, g.col_base + n0, b);
+                else tma3_prefetch(&maps.Xm, g.col_base + n0, g.row_base + k_lo + kk, b);
+            };
+            if (MODE == 1 && !no_pf)
+                for (int kb = NST; kb < NST + PF; ++kb) prefetch_x(kb);
             for (int kb = 0; kb < nkb; ++kb) {
                 const int st = kb % NST;
+                if (MODE == 1 && !no_pf && kb >= NST) prefetch_x(kb + PF);
                 if (kb >= NST) tc::mbar_wait(&empty[st], (uint32_t)((kb / NST - 1) & 1));
                 float *base = sm + st * STAGE;
                 const uint32_t bbytes = MODE == 1 && H ? IMG * 2 : IMG * 4;   // fp16 X box: half the bytes
@@ -443,7 +465,8 @@ cudaError_t launch_flat_tc(const FlatTcPlan *plan, int par, int mode, bool lq, i
                            int col_base, float *Wp, float *Gp, int64_t ws_bstride, int ns, int rps, void *a,
                            int64_t n, int64_t a_bstride, int64_t batch, cudaStream_t st) {
     using namespace ftc;
-    Args g{M, C, row_base, col_base, rps, Wp, Gp, ws_bstride, a, n, a_bstride};
+    static const int no_pf = getenv("BSVD_TC_NOPF") ? 1 : 0;
+    Args g{M, C, row_base, col_base, rps, Wp, Gp, ws_bstride, a, n, a_bstride, no_pf};
     const Maps &maps = plan->maps[par];
     dim3 grid;
     cudaError_t e;
