@@ -384,7 +384,7 @@ def run_b200(args):
     # model -- time only
     phases["diagonal"] = {"bound": "latency", "kernel": "k_slice + k_values_u (stage 3, fp64 continuant Sturm counts + Laguerre)",
                           "ms": per["diagonal"], "achieved": None, "peak": None, "frac": None,
-                          "traffic": traffic.get("k_values") if wl == "single" else None}
+                          "traffic": traffic.get("k_values_u") if wl == "single" else None}
     # the required roofline object: the largest single kernel of the step (the
     # chase is one launch, timed live by its device events)
     roof = dict(phases["bidiagonal"])

@@ -25,7 +25,8 @@ for (_, name), m in per.items():
     a["launches"] += 1
     a["bytes"] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
     a["ns"] += m.get("gpu__time_duration.sum", 0.0)
-not_s1 = {"k_chase2", "k_chase", "k_chase_cta", "k_chase_seq", "k_values", "k_slice", "k_copy_in_pad",
+not_s1 = {"k_chase2", "k_chase", "k_chase_cta", "k_chase_seq", "k_values", "k_values_u", "k_slice", "k_copy_in_pad",
+          "k_absmax", "k_unscale_values",
           "k_pack_band", "k_extract_bidiag", "k_bisect_prep", "k_clear_band"}
 out = {k: v["bytes"] / v["launches"] for k, v in agg.items()}
 out[f"stage1_step_n{n}"] = sum(v["bytes"] for k, v in agg.items() if k not in not_s1 and not k.startswith("at"))
