@@ -97,6 +97,61 @@ def test_bidiagonal_scaling_bitwise(P, be_tree):
         assert same_bits(P.bidiagonal_values(d * s, e * s, backend=be_tree), v * s)
 
 
+def _bidiag_case(case, rng):
+    if case == "clustered":      # near-multiple values (relative gaps ~1e-14)
+        n = 300
+        d = 1.0 + 1e-14 * np.arange(n)
+        e = np.full(n - 1, 1e-15)
+    elif case == "graded":       # 15 decades
+        n = 400
+        d = np.logspace(0, -15, n)
+        e = 0.5 * np.logspace(0, -15, n - 1)
+    elif case == "tiny_tail":    # values far below the bracket floor of the largest
+        n = 200
+        d = np.concatenate([rng.standard_normal(100), 1e-200 * rng.standard_normal(100)])
+        e = np.concatenate([rng.standard_normal(99), [1e-200], 1e-200 * rng.standard_normal(99)])
+    elif case == "wilkinson":    # close pairs
+        n = 201
+        d = np.abs(np.arange(n) - n // 2).astype(np.float64) + 1.0
+        e = np.ones(n - 1)
+    elif case == "huge_range":
+        n = 257
+        d = rng.standard_normal(n) * 10.0 ** rng.uniform(-30, 30, n)
+        e = rng.standard_normal(n - 1) * 10.0 ** rng.uniform(-30, 30, n - 1)
+    elif case == "rank_deficient":
+        n = 256
+        d = rng.standard_normal(n)
+        d[::3] = 0.0
+        e = rng.standard_normal(n - 1)
+    else:                        # "n2"
+        n = 2
+        d, e = np.array([1e-300, 1.0]), np.array([1e-300])
+    return d, e
+
+
+@pytest.mark.parametrize("case", ["clustered", "graded", "tiny_tail", "wilkinson", "huge_range",
+                                  "rank_deficient", "n2"])
+def test_bidiagonal_values_adversarial(P, be_tree, case):
+    """Stage 3 (k_values_u: Laguerre + ulp stencil + hunt + quartering) on
+    spectra that stress its schedule, against LAPACK on the same bidiagonal:
+    every value found, sorted, within the fp64 bound."""
+    d, e = _bidiag_case(case, np.random.default_rng(11))
+    got = P.bidiagonal_values(d, e, backend=be_tree)
+    want = np.linalg.svd(np.diag(d) + np.diag(e, 1), compute_uv=False)
+    assert got.shape == want.shape and np.all(np.isfinite(got))
+    assert np.all(np.diff(got) <= 0)
+    assert_close(got, want, np.float64, d.size, what=case)
+
+
+def test_bidiagonal_exact_multiplicities(P, be_tree):
+    """Exact multiple values (a split bidiagonal, e = 0) come back exactly:
+    the count at x equal to a value excludes it, so the bracket closes on it."""
+    k = 50
+    d = np.tile([2.0, 1.0, 0.5], k)
+    got = P.bidiagonal_values(d, np.zeros(d.size - 1), backend=be_tree)
+    assert np.array_equal(got, np.repeat([2.0, 1.0, 0.5], k))
+
+
 # ---- stage 2: chase on the reference band ----------------------------------
 
 @pytest.mark.parametrize("name", golden_names("pipe_"))
