@@ -693,7 +693,10 @@ __device__ __forceinline__ int msg_index(const int (&mc)[NC], int k) {
     return base + k / NC - (dr == 0 ? 1 : 0);
 }
 
-template <int NC, typename T>
+// DEV: the development variants (BSVD_CHASE_TRACE timestamps, the
+// BSVD_CHASE_EARLY edge reload); compiled out of the default kernel, whose
+// register budget (128 at 512 threads) they would otherwise share.
+template <int NC, typename T, bool DEV>
 __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, int64_t ld,
                                                   int64_t batch, int *flags, int fstride,
                                                   int64_t nitems, unsigned long long *trace, int strict) {
@@ -724,10 +727,10 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
         for (int k = (int)rank; k < nops; k += NC) {
             const Blk g = geom(s, k, n, b);
             unsigned long long *tr =
-                (trace && m == 0 && s < 256 && k < 32 && tid == 0) ? trace + (s * 32 + k) * 16 : nullptr;
+                (DEV && trace && m == 0 && s < 256 && k < 32 && tid == 0) ? trace + (s * 32 + k) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
             T x[4][8];
-            if (s > 0 && !(strict & 2)) {
+            if (s > 0 && (!DEV || !(strict & 2))) {
                 // sweep s-1 must have stored blocks 0..k (flag 2) and the
                 // edges of blocks k+1, k+2 (flag >= 1): the rows/columns of
                 // this block that lie in them (scripts/chase_dep_check.py);
@@ -742,7 +745,7 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
                 }
                 __syncthreads();
                 load_blk<T>(A, g, x);
-            } else if (s > 0) {
+            } else if (DEV && s > 0) {
                 // sweep s-1 must have stored blocks 0..k (flag 2) and the
                 // edges of blocks k+1, k+2 (flag >= 1): the rows/columns of
                 // this block that lie in them (scripts/chase_dep_check.py);
@@ -1203,8 +1206,10 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         lc.stream = st;
         lc.attrs = attr;
         lc.numAttrs = 1;
+        const bool dev = getenv("BSVD_CHASE_TRACE") || (getenv("BSVD_CHASE_EARLY") && atoi(getenv("BSVD_CHASE_EARLY")));
         void (*kern)(T *, int64_t, int, int64_t, int64_t, int *, int, int64_t, unsigned long long *, int) =
-            NC == 2 ? ch2::k_chase2<2, T> : (NC == 3 ? ch2::k_chase2<3, T> : ch2::k_chase2<4, T>);
+            dev ? (NC == 2 ? ch2::k_chase2<2, T, true> : (NC == 3 ? ch2::k_chase2<3, T, true> : ch2::k_chase2<4, T, true>))
+                : (NC == 2 ? ch2::k_chase2<2, T, false> : (NC == 3 ? ch2::k_chase2<3, T, false> : ch2::k_chase2<4, T, false>));
         int max_clusters = 0;
         lc.gridDim = dim3((unsigned)(want * NC));
         err = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &lc);
