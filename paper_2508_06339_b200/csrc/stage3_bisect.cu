@@ -755,7 +755,16 @@ __global__ void __launch_bounds__(128) k_values_u(const double *__restrict__ o2,
         const double xs[2] = {px[ic == 0 ? 1 : 0], px[ic == 2 ? 1 : 2]};
         double G, S2;
         int cs[2];
-        const int64_t cc = sturm_laguerre_pts<2>(ob, m, xc, xs, G, S2, cs) - n;
+        // a warp whose active lanes all run plain Laguerre passes (their extra
+        // points coincide with x_c) skips the two extra chains
+        int64_t cc;
+        if (__any_sync(0xffffffffu, !done && (!lag || stencil))) {
+            cc = sturm_laguerre_pts<2>(ob, m, xc, xs, G, S2, cs) - n;
+        } else {
+            const int c0 = sturm_laguerre(ob, m, xc, 0x1p-1000, G, S2);
+            cs[0] = cs[1] = c0;
+            cc = c0 - n;
+        }
         if (done) continue;
         ++n_pass;
         n_lag += lag;
