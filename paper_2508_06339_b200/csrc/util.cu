@@ -24,21 +24,47 @@ __device__ __forceinline__ __half scale_pow2(__half v, double sc) {
 // chase reflectors; the values are multiplied back exactly at the end.
 // Per-matrix max |a| (as the bits of a non-negative double: they order like
 // unsigned integers), for the power-of-two input normalisation.
+// Column-wise sweep (no per-element 64-bit div/mod): block x of matrix m
+// takes columns x, x + gridDim.x, ...; threads run down the column
+// (coalesced); one atomic per block after a block reduction.
 template <typename S>
-__global__ void k_absmax(const S *__restrict__ src, int64_t n, int64_t lda, int64_t sbs,
-                         unsigned long long *__restrict__ amax) {
+__global__ void __launch_bounds__(256) k_absmax(const S *__restrict__ src, int64_t n, int64_t lda, int64_t sbs,
+                                                unsigned long long *__restrict__ amax) {
+    __shared__ double red[8];
     const int64_t m = blockIdx.y;
     src += m * sbs;
     double mx = 0.0;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * n;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = idx / n, r = idx % n;
-        const double v = fabs(to_f64(src[c * lda + r]));
-        mx = v > mx ? v : mx;            // NaN never wins (the finite check reports it)
+    bool vdone = false;
+    if constexpr (sizeof(S) == 4) {
+        if ((n & 3) == 0 && (lda & 3) == 0 && ((uintptr_t)src & 15) == 0) {   // float4 sweep
+            vdone = true;
+            for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+                const float4 *col = reinterpret_cast<const float4 *>(src + c * lda);
+#pragma unroll 4
+                for (int64_t r = threadIdx.x; r < n / 4; r += blockDim.x) {
+                    const float4 v = col[r];
+                    const float t = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+                    mx = (double)t > mx ? (double)t : mx;
+                }
+            }
+        }
+    }
+    for (int64_t c = vdone ? n : blockIdx.x; c < n; c += gridDim.x) {
+        const S *col = src + c * lda;
+#pragma unroll 4
+        for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
+            const double v = fabs(to_f64(col[r]));
+            mx = v > mx ? v : mx;        // NaN never wins (the finite check reports it)
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(amax + m, (unsigned long long)__double_as_longlong(mx));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+        atomicMax(amax + m, (unsigned long long)__double_as_longlong(mx));
+    }
 }
 
 // scale = 2^(1 - e) with max|a| = f 2^e, f in [0.5, 1): max|a| * scale in [1, 2)
@@ -59,18 +85,43 @@ __global__ void k_copy_in_pad(const S *__restrict__ src, int64_t n, int64_t lda,
     dst += m * np * np;
     const double sc = amax ? pow2_scale(amax[m]) : 1.0;   // exact: a power of two
     if (unscale && blockIdx.x == 0 && threadIdx.x == 0) unscale[m] = 1.0 / sc;
-    const int64_t total = np * np;
-    bool bad = false;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = idx / np, r = idx % np;
-        S v = S(0.0f);
-        if (r < n && c < n) {
-            v = src[c * lda + r];
-            bad |= !is_finite_v(v);
-            if (amax) v = scale_pow2(v, sc);
+    bool bad = false, vdone = false;
+    if constexpr (sizeof(S) == 4) {
+        if ((n & 3) == 0 && (np & 3) == 0 && (lda & 3) == 0 && ((uintptr_t)src & 15) == 0 &&
+            ((uintptr_t)dst & 15) == 0) {                  // float4 sweep
+            vdone = true;
+            for (int64_t c = blockIdx.x; c < np; c += gridDim.x) {
+                const float4 *col = reinterpret_cast<const float4 *>(src + c * lda);
+                float4 *out = reinterpret_cast<float4 *>(dst + c * np);
+#pragma unroll 4
+                for (int64_t r = threadIdx.x; r < np / 4; r += blockDim.x) {
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (4 * r < n && c < n) {
+                        v = col[r];
+                        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+                        if (amax) {
+                            const float f = (float)sc;
+                            v.x *= f; v.y *= f; v.z *= f; v.w *= f;
+                        }
+                    }
+                    out[r] = v;
+                }
+            }
         }
-        dst[idx] = v;
+    }
+    for (int64_t c = vdone ? np : blockIdx.x; c < np; c += gridDim.x) {   // column-wise, coalesced
+        const S *col = src + c * lda;
+        S *out = dst + c * np;
+#pragma unroll 4
+        for (int64_t r = threadIdx.x; r < np; r += blockDim.x) {
+            S v = S(0.0f);
+            if (r < n && c < n) {
+                v = col[r];
+                bad |= !is_finite_v(v);
+                if (amax) v = scale_pow2(v, sc);
+            }
+            out[r] = v;
+        }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, 1);
 }
@@ -79,16 +130,16 @@ template <typename S>
 cudaError_t copy_in_pad(const S *src, int64_t n, int64_t lda, int64_t src_bstride, S *dst,
                         int64_t np, int64_t batch, int *nonfinite_flag, cudaStream_t st,
                         unsigned long long *amax, double *unscale) {
-    const int64_t total = np * np;
     if (amax) {
         cudaError_t e = cudaMemsetAsync(amax, 0, (size_t)batch * sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
-        dim3 g1((unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), (unsigned)batch);
+        // about 8 blocks per SM in total, at least one per matrix
+        dim3 g1((unsigned)std::max<int64_t>(1, std::min<int64_t>(n, 1184 / batch)), (unsigned)batch);
         k_absmax<S><<<g1, 256, 0, st>>>(src, n, lda, src_bstride, amax);
         bsvd_host::count_launch();
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 8192), (unsigned)batch);
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(np, 2368 / batch)), (unsigned)batch);
     k_copy_in_pad<S><<<grid, 256, 0, st>>>(src, n, lda, src_bstride, dst, np, nonfinite_flag, amax, unscale);
     bsvd_host::count_launch();
     return cudaGetLastError();
