@@ -40,7 +40,7 @@ constexpr double kStencilTrig = BSVD_STENCIL_TRIG;   // relative Laguerre step t
 // development instrumentation (BSVD_S3_STATS=file): per value the number of
 // isolation / Laguerre / probe / final-bisection Sturm passes
 __device__ int *g_s3stats = nullptr;
-__device__ int64_t g_s3trace = -1;   // BSVD_S3_TRACE=k: printf the passes of value k
+__device__ int64_t g_s3trace = -1;   // BSVD_S3_TRACE=k: printf the passes of value k (build -DBSVD_S3_DEBUG)
 
 // Per-matrix prep: o2[j] = (o_j * 2^-p)^2, scal = {2^p, gersh_scaled}.
 __global__ void __launch_bounds__(256) k_bisect_prep(const double *__restrict__ d,
@@ -194,6 +194,17 @@ __device__ __forceinline__ double pow2_norm(double v) {
     return __hiloint2double(0x7fe00000 - (__double2hiint(v) & 0x7ff00000), 0);
 }
 
+// The o2 stream of the step loops: block j of 8 values.  Each block's loads
+// are issued one iteration ahead (o2_load8 of j + 8 into `on`), so their
+// latency never lands on the recurrence's dependency chain however the
+// compiler schedules the iteration (a build that interleaved them with the
+// chain ran stage 3 1.5x slower).
+__device__ __forceinline__ void o2_load8(const double *__restrict__ o2, int64_t j, int64_t m, double (&o)[8]) {
+    const bool ok = j + 8 <= m;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o[u] = ok ? __ldg(o2 + j + u) : 0.0;
+}
+
 template <int K>
 __device__ __forceinline__ void negcountK(const double *__restrict__ o2, int64_t m, const double (&x)[K],
                                           double pivmin, int (&c)[K]) {
@@ -206,10 +217,11 @@ __device__ __forceinline__ void negcountK(const double *__restrict__ o2, int64_t
         c[i] = p[i] < 0.0;
     }
     int64_t j = 0;
+    double o[8];
+    o2_load8(o2, 0, m, o);
     for (; j + 8 <= m; j += 8) {
-        double o[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) o[u] = __ldg(o2 + j + u);
+        double on[8];
+        o2_load8(o2, j + 8, m, on);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
 #pragma unroll
@@ -226,12 +238,14 @@ __device__ __forceinline__ void negcountK(const double *__restrict__ o2, int64_t
             pm[i] *= s;
             p[i] *= s;
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = on[u];
     }
     for (; j < m; ++j) {
-        const double o = __ldg(o2 + j);
+        const double ot = __ldg(o2 + j);
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-            const double pn = cstep(x[i], p[i], o, pm[i]);
+            const double pn = cstep(x[i], p[i], ot, pm[i]);
             c[i] += (pn < 0.0) != (p[i] < 0.0);
             pm[i] = p[i];
             p[i] = pn;
@@ -362,14 +376,17 @@ __device__ __forceinline__ int sturm_laguerre(const double *__restrict__ o2, int
         dpm = dp; dp = dpn;
         ddpm = ddp; ddp = ddpn;
     };
+    double o[8];
+    o2_load8(o2, 0, m, o);
     for (; j + 8 <= m; j += 8) {
-        double o[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) o[u] = __ldg(o2 + j + u);
+        double on[8];
+        o2_load8(o2, j + 8, m, on);
 #pragma unroll
         for (int u = 0; u < 8; ++u) step(o[u]);
         const double s = pow2_norm(fmax(fabs(pm), fabs(p)));
         pm *= s; p *= s; dpm *= s; dp *= s; ddpm *= s; ddp *= s;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = on[u];
     }
     for (; j < m; ++j) step(__ldg(o2 + j));
     const double r = 1.0 / p;
@@ -412,10 +429,11 @@ __device__ __forceinline__ int sturm_laguerre_pts(const double *__restrict__ o2,
         }
     };
     int64_t j = 0;
+    double o[8];
+    o2_load8(o2, 0, m, o);
     for (; j + 8 <= m; j += 8) {
-        double o[8];
-#pragma unroll
-        for (int u8 = 0; u8 < 8; ++u8) o[u8] = __ldg(o2 + j + u8);
+        double on[8];
+        o2_load8(o2, j + 8, m, on);
 #pragma unroll
         for (int u8 = 0; u8 < 8; ++u8) step(o[u8]);
         const double s = pow2_norm(fmax(fabs(pm), fabs(p)));
@@ -426,6 +444,8 @@ __device__ __forceinline__ int sturm_laguerre_pts(const double *__restrict__ o2,
             qm[i] *= si;
             q[i] *= si;
         }
+#pragma unroll
+        for (int u8 = 0; u8 < 8; ++u8) o[u8] = on[u8];
     }
     for (; j < m; ++j) step(__ldg(o2 + j));
     const double r = 1.0 / p;
@@ -785,10 +805,12 @@ __global__ void __launch_bounds__(128) k_values_u(const double *__restrict__ o2,
         for (int i = 2; i >= 0; --i)
             if (i > top && px[i] > lo && px[i] < hi && pc[i] >= rank) { nhi = px[i]; nchi = pc[i]; }
         lo = nlo; hi = nhi; clo = nclo; chi = nchi;
+#ifdef BSVD_S3_DEBUG
         if (k == g_s3trace && b == 0)
             printf("pass %d lag %d st %d xc %.17g cc %lld (rank %lld) lo %.17g hi %.17g w/ulp %.3g G %.6g S2 %.6g sprev %.3g\n",
                    n_pass, (int)lag, (int)stencil, xc, (long long)cc, (long long)rank, lo, hi,
                    (hi - lo) / (0x1p-52 * fabs(hi)), G, S2, sprev);
+#endif
         const double mid = 0.5 * (lo + hi);
         if (hi <= floor_ || !(mid > lo && mid < hi)) { done = true; continue; }
         if (lag) {
