@@ -405,6 +405,14 @@ __global__ void k_extract_bidiag(const TB *__restrict__ band, int64_t n, int64_t
 // are published in block order with a release counter per sweep.
 namespace ch2 {
 constexpr int NW = 16, NTH = 512, BK = 128;
+// Tile shapes: a BKT x BKT block over BKT/8 warps, thread (w, l) holding rows
+// l + 32a (a < BKT/32) and columns w + (BKT/8) q (q < 8).  BKT = 128 serves
+// 64 < b <= 128; narrow bands use BKT = 64 / 32 (8 / 4 warps), so the
+// reductions, barriers and loads of an op scale with the band, not with 128.
+template <int BKT>
+struct Shape {
+    static constexpr int NW = BKT / 8, NTH = NW * 32, RA = BKT / 32;
+};
 
 __device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
@@ -500,28 +508,29 @@ __device__ __forceinline__ void reflector(const T *p, int L, T &tau, T &scale,
 // Register tile: thread (warp w, lane l) holds rows l + 32a (a < 4) and
 // columns w + 16q (q < 8) of the 128 x 128 block -- one coalesced 256-byte
 // column segment per (a, q).
-template <typename T>
-__device__ __forceinline__ void load_blk(const BandT<T> &A, const Blk &g, T (&x)[4][8]) {
+template <typename T, int BKT>
+__device__ __forceinline__ void load_blk(const BandT<T> &A, const Blk &g, T (&x)[Shape<BKT>::RA][8]) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const int c = w + 16 * q;
+        const int c = w + Shape<BKT>::NW * q;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < Shape<BKT>::RA; ++a) {
             const int r = l + 32 * a;
             x[a][q] = (r < g.nr && c < g.nc) ? __ldcg(A.at(g.R0 + r, g.C0 + c)) : T(0);
         }
     }
 }
 // part: 0 all, 1 row 0 only, 2 column 0 only, 3 all but row 0, 4 all but column 0
-template <typename T>
-__device__ __forceinline__ void store_blk(const BandT<T> &A, const Blk &g, const T (&x)[4][8], int part) {
+template <typename T, int BKT>
+__device__ __forceinline__ void store_blk(const BandT<T> &A, const Blk &g, const T (&x)[Shape<BKT>::RA][8],
+                                          int part) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const int c = w + 16 * q;
+        const int c = w + Shape<BKT>::NW * q;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < Shape<BKT>::RA; ++a) {
             const int r = l + 32 * a;
             const bool sel = part == 0 || (part == 1 && r == 0) || (part == 2 && c == 0) ||
                              (part == 3 && r != 0) || (part == 4 && c != 0);
@@ -588,13 +597,14 @@ __device__ __forceinline__ void lane_allreduce8(T (&part)[8]) {
 // column dots reduce over the lanes.  carrier: column 0 is the pivot column.
 // emit: row 0 after the update (the next right op's pivot) is shipped before
 // the rest of the block is updated.
-template <typename T>
-__device__ __forceinline__ void left_apply(T (&x)[4][8], const T *p, int L, T tau,
+template <typename T, int BKT>
+__device__ __forceinline__ void left_apply(T (&x)[Shape<BKT>::RA][8], const T *p, int L, T tau,
                                            T scale, T beta, bool carrier, const Emit<T> &em) {
+    constexpr int RA = Shape<BKT>::RA, NWT = Shape<BKT>::NW;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    T va[4], part[8];
+    T va[RA], part[8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
+    for (int a = 0; a < RA; ++a) {
         const int j = l + 32 * a;
         va[a] = j == 0 ? T(1) : (j < L ? p[j] * scale : T(0));
     }
@@ -603,7 +613,7 @@ __device__ __forceinline__ void left_apply(T (&x)[4][8], const T *p, int L, T ta
         for (int q = 0; q < 8; ++q) {
             T t = va[0] * x[0][q];
 #pragma unroll
-            for (int a = 1; a < 4; ++a) t = fma(va[a], x[a][q], t);
+            for (int a = 1; a < RA; ++a) t = fma(va[a], x[a][q], t);
             part[q] = t;
         }
         lane_allreduce8<T>(part);
@@ -615,17 +625,17 @@ __device__ __forceinline__ void left_apply(T (&x)[4][8], const T *p, int L, T ta
     }
     if (em.self && l == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) emit_put(em, w + 16 * q, fma(-part[q], va[0], x[0][q]));
+        for (int q = 0; q < 8; ++q) emit_put(em, w + NWT * q, fma(-part[q], va[0], x[0][q]));
     }
     if (tau != T(0)) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
 #pragma unroll
-            for (int a = 0; a < 4; ++a) x[a][q] = fma(-part[q], va[a], x[a][q]);
+            for (int a = 0; a < RA; ++a) x[a][q] = fma(-part[q], va[a], x[a][q]);
     }
     if (carrier && w == 0) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) x[a][0] = (l + 32 * a == 0) ? beta : T(0);
+        for (int a = 0; a < RA; ++a) x[a][0] = (l + 32 * a == 0) ? beta : T(0);
     }
 }
 
@@ -633,53 +643,71 @@ __device__ __forceinline__ void left_apply(T (&x)[4][8], const T *p, int L, T ta
 // row: row dots reduce over the 16 warps through shared memory.
 // carrier: row 0 is the pivot row.  emit: column 0 after the update (the
 // next left op's pivot).
-template <typename T>
-__device__ __forceinline__ void right_apply(T (&x)[4][8], const T *p, int L, T tau,
+template <typename T, int BKT>
+__device__ __forceinline__ void right_apply(T (&x)[Shape<BKT>::RA][8], const T *p, int L, T tau,
                                             T scale, T beta, bool carrier,
-                                            T (*red)[BK], T (*red2)[BK], const Emit<T> &em) {
+                                            T (*red)[BKT], T (*red2)[BKT], const Emit<T> &em) {
+    constexpr int RA = Shape<BKT>::RA, NWT = Shape<BKT>::NW;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31, tid = threadIdx.x;
-    T vq[8], td[4];
+    T vq[8], td[RA];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const int c = w + 16 * q;
+        const int c = w + NWT * q;
         vq[q] = c == 0 ? T(1) : (c < L ? p[c] * scale : T(0));
     }
     if (tau != T(0)) {                        // uniform across the CTA
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < RA; ++a) {
             T t = x[a][0] * vq[0];
 #pragma unroll
             for (int q = 1; q < 8; ++q) t = fma(x[a][q], vq[q], t);
             red[w][l + 32 * a] = t;
         }
         __syncthreads();
-        {
-            const int row = tid & (BK - 1), g = tid >> 7;
-            red2[g][row] = (red[4 * g][row] + red[4 * g + 1][row]) + (red[4 * g + 2][row] + red[4 * g + 3][row]);
-        }
-        __syncthreads();
+        if constexpr (NWT == 16) {
+            {
+                const int row = tid & (BKT - 1), g = tid >> 7;
+                red2[g][row] = (red[4 * g][row] + red[4 * g + 1][row]) + (red[4 * g + 2][row] + red[4 * g + 3][row]);
+            }
+            __syncthreads();
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int r = l + 32 * a;
-            td[a] = tau * ((red2[0][r] + red2[1][r]) + (red2[2][r] + red2[3][r]));
+            for (int a = 0; a < RA; ++a) {
+                const int r = l + 32 * a;
+                td[a] = tau * ((red2[0][r] + red2[1][r]) + (red2[2][r] + red2[3][r]));
+            }
+        } else {
+            // <= 8 warps: every thread sums its rows' NWT partials (fixed
+            // pairwise tree: every warp gets the same bits)
+#pragma unroll
+            for (int a = 0; a < RA; ++a) {
+                const int r = l + 32 * a;
+                T v[NWT];
+#pragma unroll
+                for (int u = 0; u < NWT; ++u) v[u] = red[u][r];
+#pragma unroll
+                for (int h = NWT / 2; h > 0; h >>= 1)
+#pragma unroll
+                    for (int u = 0; u < h; ++u) v[u] += v[u + h];
+                td[a] = tau * v[0];
+            }
         }
     } else {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) td[a] = T(0);
+        for (int a = 0; a < RA; ++a) td[a] = T(0);
     }
     if (em.self && w == 0) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) emit_put(em, l + 32 * a, fma(-td[a], vq[0], x[a][0]));
+        for (int a = 0; a < RA; ++a) emit_put(em, l + 32 * a, fma(-td[a], vq[0], x[a][0]));
     }
     if (tau != T(0)) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < RA; ++a)
 #pragma unroll
             for (int q = 0; q < 8; ++q) x[a][q] = fma(-td[a], vq[q], x[a][q]);
     }
     if (carrier && l == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[0][q] = (w + 16 * q == 0) ? beta : T(0);
+        for (int q = 0; q < 8; ++q) x[0][q] = (w + NWT * q == 0) ? beta : T(0);
     }
 }
 
@@ -696,15 +724,18 @@ __device__ __forceinline__ int msg_index(const int (&mc)[NC], int k) {
 // DEV: the development variants (BSVD_CHASE_TRACE timestamps, the
 // BSVD_CHASE_EARLY edge reload); compiled out of the default kernel, whose
 // register budget (128 at 512 threads) they would otherwise share.
-template <int NC, typename T, bool DEV>
-__global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, int64_t ld,
-                                                  int64_t batch, int *flags, int fstride,
-                                                  int64_t nitems, unsigned long long *trace, int strict) {
+template <int NC, typename T, bool DEV, int BKT>
+__global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t n, int b, int64_t ld,
+                                                              int64_t batch, int *flags, int fstride,
+                                                              int64_t nitems, unsigned long long *trace,
+                                                              int strict) {
+    static_assert(!DEV || BKT == 128, "the development variants assume 128 x 128 tiles");
+    constexpr int RA = Shape<BKT>::RA, NTH = Shape<BKT>::NTH, BK = BKT;
     __shared__ T piv_self[BK];
     __shared__ T piv0[BK];
     __shared__ T piv_in[2][BK];
-    __shared__ T red[NW][BK];
-    __shared__ T red2[4][BK];
+    __shared__ T red[Shape<BKT>::NW][BK];
+    __shared__ T red2[BKT == 128 ? 4 : 1][BK];
     __shared__ __align__(8) uint64_t mbar[2];
     const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
     const unsigned rank = cluster_rank();
@@ -729,7 +760,7 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
             unsigned long long *tr =
                 (DEV && trace && m == 0 && s < 256 && k < 32 && tid == 0) ? trace + (s * 32 + k) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
-            T x[4][8];
+            T x[RA][8];
             if (s > 0 && (!DEV || !(strict & 2))) {
                 // sweep s-1 must have stored blocks 0..k (flag 2) and the
                 // edges of blocks k+1, k+2 (flag >= 1): the rows/columns of
@@ -744,8 +775,9 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
                         if (spin > 64) __nanosleep(32);
                 }
                 __syncthreads();
-                load_blk<T>(A, g, x);
+                load_blk<T, BKT>(A, g, x);
             } else if (DEV && s > 0) {
+              if constexpr (DEV) {
                 // sweep s-1 must have stored blocks 0..k (flag 2) and the
                 // edges of blocks k+1, k+2 (flag >= 1): the rows/columns of
                 // this block that lie in them (scripts/chase_dep_check.py);
@@ -761,7 +793,7 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
                         if (spin > 64) __nanosleep(32);
                 }
                 __syncthreads();
-                load_blk<T>(A, g, x);
+                load_blk<T, BKT>(A, g, x);
                 uint32_t mask = 0;
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
@@ -804,8 +836,9 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
                             if ((mask >> (8 * aa + q)) & 1u)
                                 x[aa][q] = __ldcg(A.at(g.R0 + l + 32 * aa, g.C0 + w + 16 * q));
                 }
+              }
             } else {
-                load_blk<T>(A, g, x);
+                load_blk<T, BKT>(A, g, x);
             }
             if (tr) tr[1] = gtimer();
             const T *pv;
@@ -849,8 +882,8 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
                 em.remote = mapa(saddr(&piv_in[idx1 & 1][0]), (uint32_t)dr);
                 em.rbar = mapa(saddr(&mbar[idx1 & 1]), (uint32_t)dr);
             }
-            if (k & 1) left_apply<T>(x, pv, L, tau, scale, beta, false, em);
-            else right_apply<T>(x, pv, L, tau, scale, beta, false, red, red2, em);
+            if (k & 1) left_apply<T, BKT>(x, pv, L, tau, scale, beta, false, em);
+            else right_apply<T, BKT>(x, pv, L, tau, scale, beta, false, red, red2, em);
             if (tr) tr[3] = gtimer();
             if (k + 1 < nops) {
                 __syncthreads();                        // piv_self complete
@@ -858,8 +891,8 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
                 const int L1 = (k & 1) ? g.nc : g.nr;
                 reflector<T>(piv_self, L1, tau, scale, beta);
                 const Emit<T> none{nullptr, 0u, 0u};
-                if (k & 1) right_apply<T>(x, piv_self, L1, tau, scale, beta, true, red, red2, none);
-                else left_apply<T>(x, piv_self, L1, tau, scale, beta, true, none);
+                if (k & 1) right_apply<T, BKT>(x, piv_self, L1, tau, scale, beta, true, red, red2, none);
+                else left_apply<T, BKT>(x, piv_self, L1, tau, scale, beta, true, none);
             }
             if (tr) tr[5] = gtimer();
             // publish block k: its edge (row 0 of an even / Q-type block,
@@ -867,14 +900,14 @@ __global__ void __launch_bounds__(NTH, 1) k_chase2(T *band, int64_t n, int b, in
             // block k-2 / k-1 reads) first, then the rest
             {
                 const bool row_edge = !(k & 1);
-                store_blk<T>(A, g, x, row_edge ? 1 : 2);
+                store_blk<T, BKT>(A, g, x, row_edge ? 1 : 2);
                 __syncthreads();
                 if (tid == 0) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     if (tr) tr[6] = gtimer();
                     st_relaxed(fl + k, 1);
                 }
-                store_blk<T>(A, g, x, row_edge ? 3 : 4);
+                store_blk<T, BKT>(A, g, x, row_edge ? 3 : 4);
                 __syncthreads();
                 if (tid == 0) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -1201,15 +1234,26 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         attr[0].val.clusterDim.x = NC;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
-        lc.blockDim = dim3(ch2::NTH);
         lc.dynamicSmemBytes = 0;
         lc.stream = st;
         lc.attrs = attr;
         lc.numAttrs = 1;
+        // tile: the narrowest of 32 / 64 / 128 that holds the band
+        // (BSVD_CHASE_BK=128 forces the wide tile: development A/B)
+        int bkt = b <= 32 ? 32 : (b <= 64 ? 64 : 128);
+        if (const char *e = getenv("BSVD_CHASE_BK")) bkt = std::max(bkt, atoi(e) >= 128 ? 128 : (atoi(e) >= 64 ? 64 : 32));
         const bool dev = getenv("BSVD_CHASE_TRACE") || (getenv("BSVD_CHASE_EARLY") && atoi(getenv("BSVD_CHASE_EARLY")));
+        if (dev) bkt = 128;
         void (*kern)(T *, int64_t, int, int64_t, int64_t, int *, int, int64_t, unsigned long long *, int) =
-            dev ? (NC == 2 ? ch2::k_chase2<2, T, true> : (NC == 3 ? ch2::k_chase2<3, T, true> : ch2::k_chase2<4, T, true>))
-                : (NC == 2 ? ch2::k_chase2<2, T, false> : (NC == 3 ? ch2::k_chase2<3, T, false> : ch2::k_chase2<4, T, false>));
+            dev ? (NC == 2 ? ch2::k_chase2<2, T, true, 128>
+                           : (NC == 3 ? ch2::k_chase2<3, T, true, 128> : ch2::k_chase2<4, T, true, 128>))
+            : bkt == 32 ? (NC == 2 ? ch2::k_chase2<2, T, false, 32>
+                                   : (NC == 3 ? ch2::k_chase2<3, T, false, 32> : ch2::k_chase2<4, T, false, 32>))
+            : bkt == 64 ? (NC == 2 ? ch2::k_chase2<2, T, false, 64>
+                                   : (NC == 3 ? ch2::k_chase2<3, T, false, 64> : ch2::k_chase2<4, T, false, 64>))
+                        : (NC == 2 ? ch2::k_chase2<2, T, false, 128>
+                                   : (NC == 3 ? ch2::k_chase2<3, T, false, 128> : ch2::k_chase2<4, T, false, 128>));
+        lc.blockDim = dim3((unsigned)(bkt / 8 * 32));
         int max_clusters = 0;
         lc.gridDim = dim3((unsigned)(want * NC));
         err = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &lc);
