@@ -1779,7 +1779,9 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
         if (C > 0) {
             cudaEventRecord(evP, sp);
             if (!tc1) {   // T from V^T V (overlaps the first product on the update stream)
-                const int gs = (int)std::min<int64_t>(kGSplit, std::max<int64_t>(1, M / 512));
+                // >= 64 rows per split: short panels (small n) are bound by the
+                // chunk loop's latency, not by the CTA count
+                const int gs = (int)std::min<int64_t>(kGSplit, std::max<int64_t>(1, M / 64));
                 const int grps = ((M + gs - 1) / gs + KC - 1) / KC * KC;
                 k_fgram<TS><<<dim3((unsigned)gs, (unsigned)batch), kGT, (TS * (TS + 1) + TS * TS / 4) * sizeof(float), sp>>>(
                     ws, wsb, n, nsplit, M, grps, par);
@@ -1803,7 +1805,7 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
                 if (getenv("BSVD_TC_NS")) ns = std::max(1, std::min(nsplit, std::min(M / 32, atoi(getenv("BSVD_TC_NS")))));
             } else if (batch == 1) {
                 ns = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, ((tc1 ? 1 : 2) * 148 + cblk - 1) / cblk));
-                ns = std::min(ns, std::max(1, M / 256));
+                ns = std::min(ns, std::max(1, M / (tc1 ? 256 : 64)));
                 if (tc1 && getenv("BSVD_TC_NS")) ns = std::max(1, std::min(nsplit, std::min(M / 32, atoi(getenv("BSVD_TC_NS")))));
             }
             const int rps = ((M + ns - 1) / ns + (tc1 ? 31 : KC - 1)) / (tc1 ? 32 : KC) * (tc1 ? 32 : KC);
