@@ -434,6 +434,31 @@ __device__ __forceinline__ void wait_local(uint32_t a, uint32_t parity) {
         : "memory");
 }
 
+// Edge mailbox (4-byte band elements): every published edge element is also
+// written as one 64-bit word (tag << 32 | bits) with a relaxed gpu-scope store;
+// the next sweep polls the words it needs until the tag matches -- the word is
+// single-copy atomic, so the tag validates the value with no fence and no flag
+// (the edge's old store -> fence -> flag -> poll -> load hand-off).
+__device__ __forceinline__ void mbox_put(unsigned long long *p, uint32_t tag, float v) {
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long mbox_ld(const unsigned long long *p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
+__device__ __forceinline__ float mbox_get(const unsigned long long *p, uint32_t tag) {
+    unsigned long long w;
+    for (int spin = 0;; ++spin) {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+        if ((uint32_t)(w >> 32) == tag) break;
+        if (spin > 64) __nanosleep(32);
+    }
+    return __uint_as_float((uint32_t)w);
+}
+constexpr int MBX_STRIDE = 128;   // words per (sweep parity, block) edge slot
+
 template <typename T>
 struct BandT {
     T *p;
@@ -728,9 +753,12 @@ template <int NC, typename T, bool DEV, int BKT>
 __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t n, int b, int64_t ld,
                                                               int64_t batch, int *flags, int fstride,
                                                               int64_t nitems, unsigned long long *trace,
-                                                              int strict) {
+                                                              int strict, unsigned long long *mbox) {
     static_assert(!DEV || BKT == 128, "the development variants assume 128 x 128 tiles");
-    constexpr int RA = Shape<BKT>::RA, NTH = Shape<BKT>::NTH, BK = BKT;
+    constexpr int RA = Shape<BKT>::RA, NTH = Shape<BKT>::NTH, BK = BKT, NWT = Shape<BKT>::NW;
+    // the edge mailbox serves 4-byte bands (fp32 compute); fp64 keeps edge flags
+    constexpr bool MBX = !DEV && sizeof(T) == 4;
+    const bool mbx = MBX && mbox && !(strict & 1);
     __shared__ T piv_self[BK];
     __shared__ T piv0[BK];
     __shared__ T piv_in[2][BK];
@@ -768,7 +796,7 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
                 // blocks below k-NC+1 were checked for this CTA's previous block
                 const int lo = k >= NC ? k - NC + 1 : 0;
                 const int j = lo + tid;
-                if (j < min(k + 3, nprev)) {
+                if (j < min(mbx ? k + 1 : k + 3, nprev)) {
                     const int want = (j <= k || (strict & 1)) ? 2 : 1;
                     const int *f = fl - fstride + j;
                     for (int spin = 0; ld_acquire(f) < want; ++spin)
@@ -776,6 +804,68 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
                 }
                 __syncthreads();
                 load_blk<T, BKT>(A, g, x);
+                if constexpr (MBX) {
+                    if (mbx) {
+                        // the last column (even k) / last row (odd k) of this block
+                        // lies on the edges of the previous sweep's blocks k+1
+                        // (all but its last element, at index +1) and k+2 (the
+                        // last element, at index 0); everything else is in
+                        // blocks <= k (scripts/chase_dep_check.py)
+                        const int bl = b - 1;
+                        const unsigned long long *mp =
+                            mbox + ((m * 2 + ((s - 1) & 1)) * (int64_t)fstride) * MBX_STRIDE;
+                        const uint32_t tag = (uint32_t)s;
+                        // all of a thread's words are loaded at once (one round
+                        // trip), then only the ones whose tag is stale re-polled
+                        if (!(k & 1)) {
+                            if (bl < g.nc && (bl % NWT) == w) {
+                                const int q = bl / NWT;
+                                const unsigned long long *pa[RA];
+                                unsigned long long wv[RA];
+#pragma unroll
+                                for (int a = 0; a < RA; ++a) {
+                                    const int r = l + 32 * a;
+                                    const int ke = r < bl ? k + 1 : k + 2, je = r < bl ? r + 1 : 0;
+                                    pa[a] = (r < g.nr && ke < nprev) ? mp + ke * MBX_STRIDE + je : nullptr;
+                                    wv[a] = pa[a] ? mbox_ld(pa[a]) : 0ull;
+                                }
+#pragma unroll
+                                for (int a = 0; a < RA; ++a) {
+                                    if (!pa[a]) continue;
+                                    for (int spin = 0; (uint32_t)(wv[a] >> 32) != tag; ++spin) {
+                                        if (spin > 64) __nanosleep(32);
+                                        wv[a] = mbox_ld(pa[a]);
+                                    }
+#pragma unroll
+                                    for (int qq = 0; qq < 8; ++qq)
+                                        if (qq == q) x[a][qq] = (T)__uint_as_float((uint32_t)wv[a]);
+                                }
+                            }
+                        } else if (bl < g.nr && (bl & 31) == l) {
+                            const int a0 = bl >> 5;
+                            const unsigned long long *pq[8];
+                            unsigned long long wv[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int c = w + NWT * q;
+                                const int ke = c < bl ? k + 1 : k + 2, je = c < bl ? c + 1 : 0;
+                                pq[q] = (c < g.nc && ke < nprev) ? mp + ke * MBX_STRIDE + je : nullptr;
+                                wv[q] = pq[q] ? mbox_ld(pq[q]) : 0ull;
+                            }
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                if (!pq[q]) continue;
+                                for (int spin = 0; (uint32_t)(wv[q] >> 32) != tag; ++spin) {
+                                    if (spin > 64) __nanosleep(32);
+                                    wv[q] = mbox_ld(pq[q]);
+                                }
+#pragma unroll
+                                for (int a = 0; a < RA; ++a)
+                                    if (a == a0) x[a][q] = (T)__uint_as_float((uint32_t)wv[q]);
+                            }
+                        }
+                    }
+                }
             } else if (DEV && s > 0) {
               if constexpr (DEV) {
                 // sweep s-1 must have stored blocks 0..k (flag 2) and the
@@ -845,7 +935,19 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
             int L;
             if (k == 0) {
                 L = (int)min((int64_t)b, n - s - 1);
-                for (int j = tid; j < BK; j += NTH) piv0[j] = j < L ? __ldcg(A.at(s, s + 1 + j)) : T(0);
+                for (int j = tid; j < BK; j += NTH) {
+                    T v = T(0);
+                    if (j < L) {
+                        // (s, s+b) is column 0 (the edge) of the previous sweep's
+                        // block 1, index 0: from the mailbox in that mode
+                        if (MBX && mbx && s > 0 && j == b - 1 && 1 < nprev)
+                            v = (T)mbox_get(mbox + ((m * 2 + ((s - 1) & 1)) * (int64_t)fstride + 1) * MBX_STRIDE,
+                                            (uint32_t)s);
+                        else
+                            v = __ldcg(A.at(s, s + 1 + j));
+                    }
+                    piv0[j] = v;
+                }
                 __syncthreads();
                 pv = piv0;
             } else {
@@ -872,6 +974,15 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
             reflector<T>(pv, L, tau, scale, beta);
             if (tr) tr[9] = gtimer();
             if (k == 0 && tid == 0) __stcg(A.at(s, s + 1), beta);
+            if constexpr (MBX) {
+                // block k-1's (0, 0) after its carrier op (= op k) is this op's
+                // beta: publish that edge word now, ~2 us before the carrier
+                // CTA publishes the whole edge -- it is the element the next
+                // sweep's block k-3 waits for last (its (b-1, b-1))
+                if (mbx && k >= 1 && tid == 0)
+                    mbox_put(mbox + ((m * 2 + (s & 1)) * (int64_t)fstride + (k - 1)) * MBX_STRIDE, (uint32_t)(s + 1),
+                             (float)beta);
+            }
             // op k on the new block; its update yields op k+1's pivot, which is
             // shipped to the CTA holding block k+1 before the bulk update
             Emit<T> em{nullptr, 0u, 0u};
@@ -898,7 +1009,40 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
             // publish block k: its edge (row 0 of an even / Q-type block,
             // column 0 of an odd / E-type block -- the part the next sweep's
             // block k-2 / k-1 reads) first, then the rest
-            {
+            bool edge_done = false;
+            if constexpr (MBX) {
+                if (mbox) {
+                    // the edge goes to the mailbox first (no fence); the band
+                    // copy of it is published with the rest of the block
+                    unsigned long long *mp =
+                        mbox + ((m * 2 + (s & 1)) * (int64_t)fstride + k) * MBX_STRIDE;
+                    const uint32_t tag = (uint32_t)(s + 1);
+                    if (!(k & 1)) {
+                        if (l == 0 && g.nr > 0) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int c = w + NWT * q;
+                                if (c < g.nc) mbox_put(mp + c, tag, (float)x[0][q]);
+                            }
+                        }
+                    } else if (w == 0 && g.nc > 0) {
+#pragma unroll
+                        for (int a = 0; a < RA; ++a) {
+                            const int r = l + 32 * a;
+                            if (r < g.nr) mbox_put(mp + r, tag, (float)x[a][0]);
+                        }
+                    }
+                    edge_done = true;
+                }
+            }
+            if (edge_done) {
+                store_blk<T, BKT>(A, g, x, 0);
+                __syncthreads();
+                if (tid == 0) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    st_relaxed(fl + k, 2);
+                }
+            } else {
                 const bool row_edge = !(k & 1);
                 store_blk<T, BKT>(A, g, x, row_edge ? 1 : 2);
                 __syncthreads();
@@ -1213,6 +1357,8 @@ static bool chase2_used(int b, int64_t batch) {
 size_t chase_workspace_bytes(int64_t n, int bw, int64_t batch) {
     const int64_t ld = 3 * (int64_t)bw + 1;
     size_t flags = chase2_used(bw, batch) ? (size_t)batch * n * chase_max_ops(n, bw) * sizeof(int) : 0;
+    // + the edge mailbox of the fp32 cluster chase (2 sweep parities x blocks x 128 words)
+    if (flags) flags += (size_t)batch * 2 * chase_max_ops(n, bw) * ch2::MBX_STRIDE * sizeof(unsigned long long) + 16;
     return (size_t)batch * (size_t)n * ((size_t)ld * sizeof(double) + sizeof(int)) + flags + 512;
 }
 
@@ -1244,7 +1390,8 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         if (const char *e = getenv("BSVD_CHASE_BK")) bkt = std::max(bkt, atoi(e) >= 128 ? 128 : (atoi(e) >= 64 ? 64 : 32));
         const bool dev = getenv("BSVD_CHASE_TRACE") || (getenv("BSVD_CHASE_EARLY") && atoi(getenv("BSVD_CHASE_EARLY")));
         if (dev) bkt = 128;
-        void (*kern)(T *, int64_t, int, int64_t, int64_t, int *, int, int64_t, unsigned long long *, int) =
+        void (*kern)(T *, int64_t, int, int64_t, int64_t, int *, int, int64_t, unsigned long long *, int,
+                     unsigned long long *) =
             dev ? (NC == 2 ? ch2::k_chase2<2, T, true, 128>
                            : (NC == 3 ? ch2::k_chase2<3, T, true, 128> : ch2::k_chase2<4, T, true, 128>))
             : bkt == 32 ? (NC == 2 ? ch2::k_chase2<2, T, false, 32>
@@ -1280,7 +1427,15 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         int early = 0;
         if (const char *e = getenv("BSVD_CHASE_EARLY")) early = atoi(e) ? 2 : 0;
         const int strict = (getenv("BSVD_CHASE_STRICT") ? 1 : 0) | early;
-        err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, flags, fstride, nitems, trace, strict);
+        // edge mailbox after the flags (fp32 bands; BSVD_CHASE_MBOX=0: edge flags)
+        unsigned long long *mbox = nullptr;
+        if (sizeof(T) == 4 && !dev && !(getenv("BSVD_CHASE_MBOX") && !atoi(getenv("BSVD_CHASE_MBOX")))) {
+            mbox = (unsigned long long *)(((uintptr_t)(flags + (size_t)batch * n * fstride) + 15) & ~(uintptr_t)15);
+            const size_t mbytes = (size_t)batch * 2 * fstride * ch2::MBX_STRIDE * sizeof(unsigned long long);
+            err = cudaMemsetAsync(mbox, 0, mbytes, st);
+            if (err != cudaSuccess) return err;
+        }
+        err = cudaLaunchKernelEx(&lc, kern, band, n_, b_, ld_, batch_, flags, fstride, nitems, trace, strict, mbox);
         bsvd_host::count_launch();
         if (err != cudaSuccess) return err;
         if (trace) {
