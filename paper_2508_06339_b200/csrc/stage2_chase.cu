@@ -795,14 +795,18 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
                 // this block that lie in them (scripts/chase_dep_check.py);
                 // blocks below k-NC+1 were checked for this CTA's previous block
                 const int lo = k >= NC ? k - NC + 1 : 0;
-                const int j = lo + tid;
-                if (j < min(mbx ? k + 1 : k + 3, nprev)) {
+                // mailbox mode: only full flags of blocks <= k, polled by every
+                // warp itself (lane j: flag lo + j), which then loads its part
+                // of the block -- no CTA barrier between the flags and the load
+                const int j = lo + (mbx ? l : tid);
+                if (j < min(mbx ? k + 1 : k + 3, nprev) && !(strict & 16)) {
                     const int want = (j <= k || (strict & 1)) ? 2 : 1;
                     const int *f = fl - fstride + j;
                     for (int spin = 0; ld_acquire(f) < want; ++spin)
                         if (spin > 64) __nanosleep(32);
                 }
-                __syncthreads();
+                if (mbx) __syncwarp();
+                else __syncthreads();
                 load_blk<T, BKT>(A, g, x);
                 if constexpr (MBX) {
                     if (mbx) {
@@ -832,7 +836,7 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
 #pragma unroll
                                 for (int a = 0; a < RA; ++a) {
                                     if (!pa[a]) continue;
-                                    for (int spin = 0; (uint32_t)(wv[a] >> 32) != tag; ++spin) {
+                                    for (int spin = 0; (uint32_t)(wv[a] >> 32) != tag && !(strict & 32); ++spin) {
                                         if (spin > 64) __nanosleep(32);
                                         wv[a] = mbox_ld(pa[a]);
                                     }
@@ -855,7 +859,7 @@ __global__ void __launch_bounds__(Shape<BKT>::NTH, 1) k_chase2(T *band, int64_t 
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
                                 if (!pq[q]) continue;
-                                for (int spin = 0; (uint32_t)(wv[q] >> 32) != tag; ++spin) {
+                                for (int spin = 0; (uint32_t)(wv[q] >> 32) != tag && !(strict & 32); ++spin) {
                                     if (spin > 64) __nanosleep(32);
                                     wv[q] = mbox_ld(pq[q]);
                                 }
@@ -1426,7 +1430,10 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         // per block costs more than the earlier load saves) -- off by default.
         int early = 0;
         if (const char *e = getenv("BSVD_CHASE_EARLY")) early = atoi(e) ? 2 : 0;
-        const int strict = (getenv("BSVD_CHASE_STRICT") ? 1 : 0) | early;
+        // BSVD_CHASE_DIAG=16 / 32 / 48: skip the block-flag / mailbox waits
+        // (wrong values -- a timing diagnostic of which dependency binds)
+        const int diag = getenv("BSVD_CHASE_DIAG") ? (atoi(getenv("BSVD_CHASE_DIAG")) & 48) : 0;
+        const int strict = (getenv("BSVD_CHASE_STRICT") ? 1 : 0) | early | diag;
         // edge mailbox after the flags (fp32 bands; BSVD_CHASE_MBOX=0: edge flags)
         unsigned long long *mbox = nullptr;
         if (sizeof(T) == 4 && !dev && !(getenv("BSVD_CHASE_MBOX") && !atoi(getenv("BSVD_CHASE_MBOX")))) {
