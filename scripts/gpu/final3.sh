@@ -8,7 +8,7 @@ python scripts/verify_configs.py > gpurun_out/vc.txt 2>&1
 python scripts/traffic_capture.py 8192 > gpurun_out/traffic.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_8192_r02c.csv python scripts/prof_one.py 8192 > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_1024_ts32_r02c.csv python scripts/prof_one.py 1024 fp32 32 > /dev/null 2>&1
-for spec in "k_values_u:0:8192:fp32:0" "k_chase2:0:1024:fp32:32" "k_fgram:10:1024:fp32:32"; do
+for spec in "k_chase2:0:8192:fp32:0" "k_chase2:0:1024:fp32:32"; do
 IFS=: read k s n dt ts <<< "$spec"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -s $s -c 1 -f -o /tmp/reps/f_${k}_${n} python scripts/prof_one.py $n $dt $ts > /dev/null 2>&1
 python scripts/ncu_summary.py /tmp/reps/f_${k}_${n}.ncu-rep > gpurun_out/sum_${k}_${n}.txt

@@ -22,6 +22,9 @@ def errs(got, want):
 
 
 def timed(fn):
+    """Wall time of one call after one warm-up call (workspace growth, module
+    load and first-touch costs stay out of the number)."""
+    fn()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     out = fn()

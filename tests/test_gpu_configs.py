@@ -209,3 +209,28 @@ def test_tensor_core_path_batched(P, oracle, dtype):
     got = P.svdvals_batched(a, P.KernelConfig(tilesize=128))
     for i in range(3):
         assert_close(got[i], oracle.svdvals(a[i].T.copy(), 128), dtype, 300, what=f"member {i}")
+
+
+@pytest.mark.parametrize("n,ts,dtype", [(1024, 128, "float32"), (1000, 64, "float32"),
+                                        (777, 32, "float16"), (2048, 128, "float32")])
+def test_chase_edge_mailbox_bitwise(P, torch, monkeypatch, n, ts, dtype):
+    """The fp32 cluster chase hands the edges to the next sweep through the tagged
+    mailbox; the edge-flag protocol (BSVD_CHASE_MBOX=0) moves the same values, so
+    both give the same bits."""
+    a = _gauss(torch, n, 7 + n, getattr(torch, dtype))
+    cfg = P.KernelConfig(tilesize=ts)
+    got = P.svdvals(a, cfg).cpu().numpy()
+    monkeypatch.setenv("BSVD_CHASE_MBOX", "0")
+    ref = P.svdvals(a, cfg).cpu().numpy()
+    assert np.array_equal(got, ref), f"mailbox vs flags differ: n={n} ts={ts} {dtype}"
+
+
+@pytest.mark.parametrize("n,ts", [(640, 32), (900, 64)])
+def test_chase_wide_tile_on_narrow_band_vs_oracle(P, oracle, monkeypatch, n, ts):
+    """Narrow bands run 32 / 64-wide chase tiles; the 128-wide tile
+    (BSVD_CHASE_BK=128) on the same band stays within tolerance of the oracle."""
+    a = np.random.default_rng(n).standard_normal((n, n)).astype(np.float32)
+    want = oracle.svdvals(a, ts)
+    assert_close(P.svdvals(a, P.KernelConfig(tilesize=ts)), want, np.float32, n, what=f"tile n={n} ts={ts}")
+    monkeypatch.setenv("BSVD_CHASE_BK", "128")
+    assert_close(P.svdvals(a, P.KernelConfig(tilesize=ts)), want, np.float32, n, what=f"tile128 n={n} ts={ts}")
