@@ -1212,17 +1212,23 @@ __device__ __forceinline__ void right_t(Tile<T, BK, NW> &x, const T *p, int L, T
             red[w * BK + l + 32 * a] = t;
         }
         __syncthreads();
-#pragma unroll
-        for (int a = 0; a < RA; ++a) {
-            const int r = l + 32 * a;
+        // reduce-scatter: thread r sums row r's NW partials once (the same
+        // order as a per-thread sum), then every thread reads its RA row sums:
+        // RA (+ NW for BK threads) shared loads per thread instead of RA * NW
+        T *rsum = red + 2 * NW * BK;
+        if ((int)threadIdx.x < BK) {
             T d = T(0);
 #pragma unroll
-            for (int g = 0; g < NW; ++g) d += red[g * BK + r];
-            const T td = tau * d;
+            for (int g = 0; g < NW; ++g) d += red[g * BK + threadIdx.x];
+            rsum[threadIdx.x] = d;
+        }
+        __syncthreads();                   // also orders these reads of red before the next op's writes
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            const T td = tau * rsum[l + 32 * a];
 #pragma unroll
             for (int q = 0; q < CQ; ++q) x.v[a][q] = fma(-td, vq[q], x.v[a][q]);
         }
-        __syncthreads();                   // red is reused by the next right op
     }
     if (carrier && l == 0) {
 #pragma unroll
@@ -1256,23 +1262,28 @@ __device__ __forceinline__ void right_t2(Tile<T, BK, NW> &x0, Tile<T, BK, NW> &x
             red[(NW + w) * BK + l + 32 * a] = t1;
         }
         __syncthreads();
+        // reduce-scatter over the 2 BK rows (thread t: block t / BK, row t % BK),
+        // then each thread reads its 2 RA row sums
+        static_assert(2 * BK <= NW * 32, "one thread per row sum");
+        T *rsum = red + 2 * NW * BK;
+        if ((int)threadIdx.x < 2 * BK) {
+            const int blk = threadIdx.x / BK, r = threadIdx.x % BK;
+            T d = T(0);
+#pragma unroll
+            for (int g = 0; g < NW; ++g) d += red[(blk * NW + g) * BK + r];
+            rsum[threadIdx.x] = d;
+        }
+        __syncthreads();                   // also orders these reads of red before the next op's writes
 #pragma unroll
         for (int a = 0; a < RA; ++a) {
             const int r = l + 32 * a;
-            T d0 = T(0), d1 = T(0);
-#pragma unroll
-            for (int g = 0; g < NW; ++g) {
-                d0 += red[g * BK + r];
-                d1 += red[(NW + g) * BK + r];
-            }
-            const T td0 = tau * d0, td1 = tau * d1;
+            const T td0 = tau * rsum[r], td1 = tau * rsum[BK + r];
 #pragma unroll
             for (int q = 0; q < CQ; ++q) {
                 x0.v[a][q] = fma(-td0, vq[q], x0.v[a][q]);
                 x1.v[a][q] = fma(-td1, vq[q], x1.v[a][q]);
             }
         }
-        __syncthreads();                   // red is reused by the next right op
     }
     if (l == 0) {
 #pragma unroll
@@ -1286,7 +1297,7 @@ __global__ void __launch_bounds__(NW * 32) k_chase_cta(T *band, int64_t n, int b
     using TL = Tile<T, BK, NW>;
     constexpr int RA = TL::RA, CQ = TL::CQ;
     __shared__ T piv[BK];
-    __shared__ T red[2 * NW * BK];
+    __shared__ T red[2 * NW * BK + 2 * BK];   // partial row dots | row sums
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int64_t m = blockIdx.x; m < batch; m += gridDim.x) {
         const ch2::BandT<T> A{band + m * n * ld, n, ld, b};
