@@ -1781,7 +1781,8 @@ static cudaError_t run_flat(S *a, int64_t n, int64_t batch, int64_t a_bstride, f
             if (!tc1) {   // T from V^T V (overlaps the first product on the update stream)
                 // >= 64 rows per split: short panels (small n) are bound by the
                 // chunk loop's latency, not by the CTA count
-                const int gs = (int)std::min<int64_t>(kGSplit, std::max<int64_t>(1, M / 64));
+                // (batches: the matrices fill the GPU; one 512-row split each)
+                const int gs = (int)std::min<int64_t>(kGSplit, std::max<int64_t>(1, M / (batch > 1 ? 512 : 64)));
                 const int grps = ((M + gs - 1) / gs + KC - 1) / KC * KC;
                 k_fgram<TS><<<dim3((unsigned)gs, (unsigned)batch), kGT, (TS * (TS + 1) + TS * TS / 4) * sizeof(float), sp>>>(
                     ws, wsb, n, nsplit, M, grps, par);
