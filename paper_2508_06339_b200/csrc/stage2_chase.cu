@@ -1444,6 +1444,14 @@ static cudaError_t launch_chase2(T *band, int64_t n, int b, int64_t ld, int64_t 
         // BSVD_CHASE_DIAG=16 / 32 / 48: skip the block-flag / mailbox waits
         // (wrong values -- a timing diagnostic of which dependency binds)
         const int diag = getenv("BSVD_CHASE_DIAG") ? (atoi(getenv("BSVD_CHASE_DIAG")) & 48) : 0;
+        if (diag) {
+            static bool warned = false;
+            if (!warned) {
+                warned = true;
+                fprintf(stderr, "bsvd: BSVD_CHASE_DIAG=%d skips chase dependencies -- the values are WRONG "
+                                "(timing diagnostic only)\n", diag);
+            }
+        }
         const int strict = (getenv("BSVD_CHASE_STRICT") ? 1 : 0) | early | diag;
         // edge mailbox after the flags (fp32 bands; BSVD_CHASE_MBOX=0: edge flags)
         unsigned long long *mbox = nullptr;
