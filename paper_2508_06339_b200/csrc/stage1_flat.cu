@@ -1132,7 +1132,16 @@ struct LdKM {
             float4 acc = f4zero();
             if (id < KC * W / 4 && k0 + k < kmax && m0 + m4 < mmax) {
                 const float *s0 = src + (int64_t)(k0 + k) * ld + m0 + m4;
-                for (int s = 0; s < cnt; ++s) {
+                // four partials in flight per round trip, summed in split order
+                int s = 0;
+                for (; s + 4 <= cnt; s += 4) {
+                    float4 v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = ld4(s0 + (int64_t)(s + u) * sstride);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+                }
+                for (; s < cnt; ++s) {
                     const float4 v = ld4(s0 + (int64_t)s * sstride);
                     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
                 }
@@ -1470,7 +1479,11 @@ k_fgram(float *ws0, int64_t ws_bstride, int64_t n, int nsplit, int M, int rps, i
     for (int e = threadIdx.x; e < TS * TS; e += kGT) {
         const int i = e / TS, j = e % TS;   // G(i, j), i < j kept (strict upper)
         float sum = 0.f;
-        for (int s = 0; s < ns; ++s) sum += __ldcg(&w.Gp[(int64_t)s * TS * TS + e]);
+        float v[kGSplit];            // all partials in flight, summed in split order
+#pragma unroll
+        for (int s = 0; s < kGSplit; ++s) v[s] = s < ns ? __ldcg(&w.Gp[(int64_t)s * TS * TS + e]) : 0.f;
+#pragma unroll
+        for (int s = 0; s < kGSplit; ++s) if (s < ns) sum += v[s];
         Tsm[j * LDT + i] = (i < j) ? sum : 0.f;
     }
     __syncthreads();
