@@ -489,3 +489,16 @@ def test_concurrent_calls_from_threads(P, oracle, dtype, ts):
         t.join()
     for i in range(4):
         assert_close(out[i], oracle.svdvals(mats[i], ts), dtype, 384, what=f"thread {i}")
+
+
+@pytest.mark.parametrize("dtype,n,ts", [("float32", 640, 64), ("float32", 1024, 128), ("float64", 384, 32)])
+@pytest.mark.parametrize("k", [30, -40])
+def test_normalisation_bypass_same_bits(P, dtype, n, ts, k):
+    """Inputs with max|a| in [2^-24, 2^24] skip the power-of-two normalisation;
+    a * 2^k (outside that range) is normalised.  Power-of-two scaling commutes
+    with the arithmetic, so the values agree bit for bit (util.cu input_scale)."""
+    a = np.random.default_rng(n + k).standard_normal((n, n)).astype(dtype)
+    cfg = P.KernelConfig(tilesize=ts)
+    base = P.svdvals(a, cfg)
+    scaled = P.svdvals(a * np.asarray(2.0 ** k, dtype=dtype), cfg)
+    assert same_bits(scaled, base * np.asarray(2.0 ** k, dtype=base.dtype)), f"{dtype} n={n} 2^{k}"
